@@ -1,0 +1,264 @@
+/*
+ * arches.h -- C ABI of the B200-native ARCHES uplink channel-estimation hot path.
+ *
+ * The reference (`/root/reference/pkg/src/ranswitch`, pure Python) has no FFI;
+ * its drop-in boundary is the Python call surface that `Pipeline.run_slot`
+ * (phy_pipeline.py:422-493) and `harness.execute_run` (harness.py:174-231)
+ * bind by name.  Each entry point below names the reference
+ * function(s) it replaces.  All pointers are DEVICE pointers unless a
+ * parameter says "host".  Complex values are interleaved float2 (complex64);
+ * scalars, features and accumulators are fp64.  No entry point allocates on
+ * the hot path: callers own every buffer (sizes via arches_*_bytes).  Every
+ * call returns an ARCHES_* status; arches_last_error() gives the thread-local
+ * message.  Plans are immutable after creation and may be shared across
+ * threads; work is enqueued on the caller's cudaStream_t (NULL = legacy).
+ *
+ * Device layouts (unit u = stream * n_slots + slot; a stream is one
+ * single-layer DMRS port of one cell; A antennas, T symbols, D DMRS symbols,
+ * N = 12*n_prb subcarriers, M = N/2 comb positions):
+ *   y        [u][A][T][N]   received grid, frequency-contiguous rows
+ *   tx       [u][T][N]      known transmitted grid (genie, equaliser SINR)
+ *   pilots   [stream][M][D] unit-magnitude DMRS pilots
+ *   h_mmse   [u][A][D][N]   MMSE expert output
+ *   h_ai     [u][A][D][N]   AI-expert (delay-truncation denoiser) output
+ */
+#ifndef ARCHES_H_
+#define ARCHES_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* arches_stream_t; /* == cudaStream_t */
+
+/* status codes: 1:1 with validation.py:9-26 plus CUDA failures */
+#define ARCHES_OK 0
+#define ARCHES_E_CONFIG 1    /* ConfigurationError */
+#define ARCHES_E_CONTRACT 2  /* ContractViolation */
+#define ARCHES_E_ESTIMATOR 3 /* EstimatorError */
+#define ARCHES_E_STATE 4     /* PipelineStateError */
+#define ARCHES_E_CUDA 5      /* CUDA runtime error */
+
+#define ARCHES_MAX_ANT 64
+#define ARCHES_MAX_DMRS 4
+#define ARCHES_MAX_SYM 14
+#define ARCHES_MAX_BINS 64 /* analysis bins: max(truncation, noise_guard, 8) */
+#define ARCHES_MAX_MCS 32
+#define ARCHES_MAX_TREE_NODES 64
+#define ARCHES_MAX_PENDING 8
+
+enum { ARCHES_EXEC_CONCURRENT = 0, ARCHES_EXEC_SELECTED_ONLY = 1 };
+enum { ARCHES_POLICY_ORACLE = 0, ARCHES_POLICY_FIXED = 1, ARCHES_POLICY_TREE = 2 };
+enum { ARCHES_TRIGGER_POLICY = 0, ARCHES_TRIGGER_FAILSAFE = 1, ARCHES_TRIGGER_ORACLE = 2,
+       ARCHES_TRIGGER_FIXED = 3 };
+
+/* SlotGeometry (radio_scene.py:30-63) */
+typedef struct arches_geom {
+  int32_t n_ant;
+  int32_t n_prb;
+  int32_t n_sym;
+  int32_t n_dmrs;
+  int32_t dmrs_symbols[ARCHES_MAX_DMRS];
+  double slot_duration_us;
+} arches_geom;
+
+/* PipelineConfig (phy_pipeline.py:353-374) + MMSE prior (ScenarioConfig.
+ * assumed_delay_spread) + Dapp/LatencyModel (dapp_control.py:26-68) */
+typedef struct arches_params {
+  int32_t noise_guard;          /* estimate_noise_var guard (expert_bank.py:199) */
+  int32_t truncation;           /* denoiser taps (expert_bank.py:182) */
+  int32_t mmse_block_prbs;      /* mmse_estimate block (expert_bank.py:154,166) */
+  int32_t window_length;        /* MAC/LCID4 throughput windows */
+  double assumed_delay_spread;  /* MMSE PDP prior */
+  double ridge;                 /* RIDGE, expert_bank.py:19 */
+  double sinr_cap_db;
+  double lcid4_fraction;
+  double lcid4_jitter;
+  double crc_margin_db;
+  double crc_scale_db;
+  int32_t mac_header_bytes;
+  int32_t n_mcs;
+  double mcs_threshold_db[ARCHES_MAX_MCS];
+  int32_t mcs_qam[ARCHES_MAX_MCS];
+  double mcs_rate[ARCHES_MAX_MCS];
+  int32_t exec_mode;            /* ARCHES_EXEC_* */
+  int32_t policy;               /* ARCHES_POLICY_* */
+  int32_t fixed_mode;           /* policy == FIXED */
+  int32_t decision_period_slots;
+  int32_t dapp_window_slots;
+  int32_t reserved0;
+  int64_t decision_delay_ns;    /* LatencyModel.decision_delay_ns() */
+  int64_t failsafe_timeout_ns;  /* DappConfig.timeout_ns() */
+  uint64_t crc_purpose_key;     /* blake2b-64("crc"), rng.py:17-21 */
+} arches_params;
+
+/* depth-limited tree node (switch_policy.py:63-98); feature < 0 = leaf */
+typedef struct arches_tree_node {
+  int32_t feature;
+  int32_t left;
+  int32_t right;
+  int32_t label;
+  double threshold;
+} arches_tree_node;
+
+typedef struct arches_tree {
+  int32_t n_nodes;
+  int32_t reserved;
+  arches_tree_node nodes[ARCHES_MAX_TREE_NODES];
+} arches_tree;
+
+/* per unit telemetry of BOTH experts; index 0 = AI (ExpertId.AI), 1 = MMSE */
+typedef struct arches_telemetry {
+  double sigma2_hat;            /* estimate_noise_var */
+  double abs_mean[2];           /* mean |H| (run_slot :454) */
+  double rsrp[2];               /* mean |H|^2 (run_slot :455) */
+  double sinr_db[2];            /* equalize (phy_pipeline.py:253-279) */
+  int32_t mcs[2];
+  int32_t tb_bytes[2];
+  int32_t num_cb[2];
+  int32_t crc[2];
+  int32_t mac_rx[2];
+  int32_t lcid4_rx[2];
+} arches_telemetry;
+
+/* KpmRecord (phy_pipeline.py:291-310) + the slot outcome extras */
+typedef struct arches_kpm {
+  int64_t slot_index;
+  double phy_throughput;
+  double rsrp;
+  double code_rate;
+  double snr_db;
+  double mac_throughput;
+  double lcid4_throughput;
+  double est_abs_mean;
+  int32_t mcs_index;
+  int32_t pdu_length;
+  int32_t ndi;
+  int32_t qam_order;
+  int32_t num_cb;
+  int32_t tb_size;
+  int32_t mac_rx_bytes;
+  int32_t lcid4_rx_bytes;
+  int32_t mode;                 /* active expert of the slot (1 MMSE, 0 AI) */
+  int32_t crc_pass;
+} arches_kpm;
+
+/* control message log entry (ControlMessage, phy_pipeline.py:43-52) */
+typedef struct arches_message {
+  int64_t decided_at_ns;
+  int64_t deliverable_at_ns;
+  int32_t mode;
+  int32_t trigger;              /* ARCHES_TRIGGER_* */
+} arches_message;
+
+typedef struct arches_plan arches_plan;
+
+/* ---- plan ---------------------------------------------------------- */
+int arches_plan_create(const arches_geom* geom, const arches_params* params,
+                       arches_plan** out);
+int arches_plan_destroy(arches_plan* plan);
+/* bytes of the caller-owned per-stream control state (windows, queues) */
+size_t arches_state_bytes(const arches_plan* plan, int32_t n_streams);
+/* scratch bytes for a batch of n_units stream-slots */
+size_t arches_workspace_bytes(const arches_plan* plan, int32_t n_units);
+/* reset control state of n_streams streams (ModeVar default 1, fixed-policy
+ * force at t=0 as harness.py:186-189).  Replaces Pipeline.__init__ state. */
+int arches_state_init(const arches_plan* plan, void* state, int32_t n_streams,
+                      arches_stream_t stream);
+
+/* ---- K1: LS front end + delay-domain analysis -----------------------
+ * Replaces ls_estimate (expert_bank.py:96-116), estimate_noise_var (:199-214)
+ * and the noise-dependent half of mmse_estimate/_wiener_matrix (:139-177) and
+ * denoiser_estimate (:182-196): comb Y/X, 20-bin comb DFT, Parseval tail
+ * power -> sigma2_hat, per-unit Wiener taps and AI taps (written to ws). */
+int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                      const void* y, const void* pilots, double* sigma2_hat, void* ws,
+                      arches_stream_t stream);
+
+/* ---- K2: expert synthesis + switch telemetry + equaliser ------------
+ * Replaces the synthesis of mmse_estimate/denoiser_estimate, the |H| and
+ * |H|^2 reductions of run_slot (:453-455) and equalize (:253-279) for BOTH
+ * experts in one pass over y/tx, then (last CTA per unit) link adaptation,
+ * transport block, Philox CRC and LCID4 split for both candidates
+ * (phy_pipeline.py:192-222,462-470).  Writes h_mmse, h_ai, tel. */
+int arches_experts_equalize(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                            const void* y, const void* tx, const double* noise_var,
+                            const uint64_t* seeds, int64_t first_slot, void* h_mmse,
+                            void* h_ai, arches_telemetry* tel, void* ws,
+                            arches_stream_t stream);
+
+/* ---- K4: per-stream sequential KPM windows + control plane ----------
+ * Replaces the order-dependent tail of run_slot (:471-488: windows, NDI,
+ * cumulative PHY rate), SwitchController.begin_slot (:123-139),
+ * Dapp.on_indication + window_features + predict (dapp_control.py:85-120,
+ * switch_policy.py:237-248), FailsafeMonitor (dapp_control.py:123-144) and
+ * the oracle/fixed message sources of execute_run (harness.py:186-226).
+ * regime may be NULL unless policy == ORACLE (1 = good).  Writes kpm (which
+ * carries the switch predicate `mode` of every slot) and appends to msg_log
+ * (capacity msg_cap per stream; msg_count[stream] is advanced). */
+int arches_kpm_scan(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                    const arches_telemetry* tel, const int8_t* regime, const arches_tree* tree,
+                    void* state, arches_kpm* kpm, arches_message* msg_log,
+                    int32_t* msg_count, int32_t msg_cap, arches_stream_t stream);
+
+/* K1 + K2 + K4 for one batch (the per-step hot path). */
+int arches_run_batch(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                     int64_t first_slot, const void* y, const void* tx, const void* pilots,
+                     const double* noise_var, const uint64_t* seeds, const int8_t* regime,
+                     const arches_tree* tree, void* state, void* h_mmse, void* h_ai,
+                     arches_telemetry* tel, arches_kpm* kpm, arches_message* msg_log,
+                     int32_t* msg_count, int32_t msg_cap, void* ws, arches_stream_t stream);
+
+/* ---- K5: zero-gap switch, reference aliasing semantics ---------------
+ * switch_select (phy_pipeline.py:81-91): for every unit whose kpm.mode == 1
+ * copy the MMSE output into the AI (downstream) buffer; mode 0 is a no-op. */
+int arches_switch_copy(const arches_plan* plan, int32_t n_units, const arches_kpm* kpm,
+                       const void* h_mmse, void* h_ai, arches_stream_t stream);
+/* single-buffer form: copy n complex values when *mode == 1 (device int) */
+int arches_switch_copy_one(const int32_t* mode, const void* src, void* dst, size_t n,
+                           arches_stream_t stream);
+
+/* ---- per-call drop-in forms (compat layer) -------------------------- */
+/* ls_estimate: materialise the comb-filled LS grid ls[u][A][D][N] */
+int arches_ls_materialize(const arches_plan* plan, int32_t n_units, const void* y,
+                          const void* pilots, void* ls, arches_stream_t stream);
+/* estimate_noise_var / mmse_estimate / denoiser_estimate from an LS grid
+ * ls[u][A][D][N]; which: 0 = noise var only, 1 = MMSE (noise_var_in[u] >= 0
+ * overrides sigma2_hat), 2 = denoiser (general N-point analysis) */
+int arches_expert_from_ls(const arches_plan* plan, int32_t n_units, int32_t which,
+                          const void* ls, const double* noise_var_in, double* sigma2_hat,
+                          void* out, void* ws, arches_stream_t stream);
+/* equalize(rx, est, noise_var, tx): est[u][A][D][N]; writes sinr_db[u] and,
+ * when x_hat != NULL, x_hat[u][T][N] */
+int arches_equalize(const arches_plan* plan, int32_t n_units, const void* y, const void* est,
+                    const void* tx, const double* noise_var, double* sinr_db,
+                    double* abs_mean, double* rsrp, void* x_hat, void* ws,
+                    arches_stream_t stream);
+/* window_features: column means of rows[n_rows][10] (sequential fp64 sum) */
+int arches_window_features(const double* rows, int32_t n_rows, double* out,
+                           arches_stream_t stream);
+/* predict: labels[i] for x[n][n_features] */
+int arches_tree_predict(const arches_tree* tree, const double* x, int32_t n, int32_t n_features,
+                        int32_t* labels, arches_stream_t stream);
+
+/* ---- host helpers (no GPU required) ---------------------------------- */
+const char* arches_last_error(void);
+const char* arches_version(void);
+/* stream(seed, "crc", slot).random() (rng.py:24-34, phy_pipeline.py:221) */
+double arches_host_crc_uniform(uint64_t seed, uint64_t purpose_key, uint64_t slot);
+/* _lcid4_jitter(slot) (phy_pipeline.py:347-350) */
+double arches_host_lcid4_jitter(uint64_t slot);
+/* blake2b-64 of an arbitrary byte string (rng.py:17-21) */
+uint64_t arches_host_blake2b64(const void* data, size_t len);
+/* analysis bins the plan computes per (a, d) */
+int32_t arches_plan_bins(const arches_plan* plan);
+/* 1 if a CUDA device is usable from this process */
+int32_t arches_device_available(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARCHES_H_ */

@@ -1,0 +1,586 @@
+// C ABI of the ARCHES B200 hot path: plan construction, launch wrappers and
+// host helpers.  See include/arches.h for the contract of every entry point.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <complex>
+#include <vector>
+
+#include "common.cuh"
+#include "k_analyze.cuh"
+#include "k_control.cuh"
+#include "k_synth_eq.cuh"
+#include "rng.cuh"
+
+#define ARCHES_VERSION "arches-b200 0.1 (sm_100a)"
+
+static thread_local char g_err[512];
+
+static int set_err(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(ARCHES_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),   \
+                     __FILE__, __LINE__);                                               \
+  } while (0)
+
+#define LAUNCH_CHECK()                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(ARCHES_E_CUDA, "launch: %s (%s:%d)", cudaGetErrorString(e_),       \
+                     __FILE__, __LINE__);                                               \
+  } while (0)
+
+struct arches_plan {
+  arches_geom g;
+  arches_params p;
+  PlanDev dev;
+  int k1_chunk;     // K1 points per chunk
+  int k1_per_chunk; // blocked MMSE: per-block bins
+  size_t k1_smem;
+  size_t k1_full_smem;  // N-point (denoiser compat) variant
+  int k1_full_chunk;
+  size_t k2_smem;
+  void* dev_tables;
+};
+
+static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ------------------------------------------------------------ workspace
+struct WsLayout {
+  size_t coef, parts, counters, block_bins, sigma2, total;
+};
+
+static WsLayout ws_layout(const arches_plan* P, int n_units) {
+  const PlanDev& d = P->dev;
+  WsLayout w;
+  size_t off = 0;
+  w.coef = off;
+  off += align256((size_t)n_units * coef_floats2(d) * sizeof(float2));
+  w.parts = off;
+  off += align256((size_t)n_units * d.n_tiles * sizeof(TilePartial));
+  w.counters = off;
+  off += align256((size_t)n_units * sizeof(unsigned int));
+  w.block_bins = off;
+  if (P->k1_per_chunk) off += align256((size_t)n_units * d.n_blocks * d.A * d.D * 8 * sizeof(double2));
+  w.sigma2 = off;
+  off += align256((size_t)n_units * sizeof(double));
+  w.total = off;
+  return w;
+}
+
+template <class T>
+static T* ws_at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(ws) + off);
+}
+
+// ------------------------------------------------------------ plan
+static void time_interp(const arches_geom& g, PlanDev& d) {
+  // _time_interp_weights (phy_pipeline.py:227-242)
+  const int D = g.n_dmrs;
+  for (int s = 0; s < ARCHES_MAX_SYM; ++s) {
+    for (int j = 0; j < ARCHES_MAX_DMRS; ++j) d.tw[s][j] = 0.f;
+    d.tw_d0[s] = d.tw_d1[s] = -1;
+    d.tw_w0[s] = d.tw_w1[s] = 0.f;
+    d.is_dmrs[s] = -1;
+  }
+  for (int j = 0; j < D; ++j) d.is_dmrs[g.dmrs_symbols[j]] = j;
+  for (int s = 0; s < g.n_sym; ++s) {
+    const double xs = s;
+    if (xs <= g.dmrs_symbols[0]) {
+      d.tw_d0[s] = 0;
+      d.tw_w0[s] = 1.f;
+    } else if (xs >= g.dmrs_symbols[D - 1]) {
+      d.tw_d0[s] = D - 1;
+      d.tw_w0[s] = 1.f;
+    } else {
+      int k = 0;
+      while (k + 1 < D && g.dmrs_symbols[k + 1] <= s) ++k;
+      const double w = (xs - g.dmrs_symbols[k]) / (double)(g.dmrs_symbols[k + 1] - g.dmrs_symbols[k]);
+      d.tw_d0[s] = k;
+      d.tw_w0[s] = (float)(1.0 - w);
+      d.tw_d1[s] = k + 1;
+      d.tw_w1[s] = (float)w;
+    }
+    if (d.tw_d0[s] >= 0) d.tw[s][d.tw_d0[s]] = d.tw_w0[s];
+    if (d.tw_d1[s] >= 0) d.tw[s][d.tw_d1[s]] = d.tw_w1[s];
+  }
+}
+
+extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* params,
+                                  arches_plan** out) {
+  if (!geom || !params || !out) return set_err(ARCHES_E_CONTRACT, "null argument");
+  const arches_geom& g = *geom;
+  const arches_params& p = *params;
+  if (g.n_ant < 1 || g.n_prb < 1 || g.n_sym < 1 || g.n_dmrs < 1)
+    return set_err(ARCHES_E_CONFIG, "geometry dimensions must be positive");
+  if (g.n_ant > ARCHES_MAX_ANT) return set_err(ARCHES_E_CONFIG, "n_ant > %d", ARCHES_MAX_ANT);
+  if (g.n_sym > ARCHES_MAX_SYM || g.n_dmrs > ARCHES_MAX_DMRS)
+    return set_err(ARCHES_E_CONFIG, "n_sym <= %d and n_dmrs <= %d required", ARCHES_MAX_SYM,
+                   ARCHES_MAX_DMRS);
+  for (int j = 0; j < g.n_dmrs; ++j) {
+    if (g.dmrs_symbols[j] < 0 || g.dmrs_symbols[j] >= g.n_sym ||
+        (j && g.dmrs_symbols[j] <= g.dmrs_symbols[j - 1]))
+      return set_err(ARCHES_E_CONFIG, "dmrs_symbols must be strictly increasing and < n_sym");
+  }
+  if (!(g.slot_duration_us > 0)) return set_err(ARCHES_E_CONFIG, "slot_duration_us must be > 0");
+  const int N = 12 * g.n_prb, M = 6 * g.n_prb;
+  if (p.noise_guard < 1 || p.noise_guard >= M)
+    return set_err(ARCHES_E_CONFIG, "guard %d outside 1..%d", p.noise_guard, M - 1);
+  if (p.truncation < 1 || p.truncation > N)
+    return set_err(ARCHES_E_CONFIG, "truncation %d outside 1..%d", p.truncation, N);
+  if (p.truncation > ARCHES_MAX_BINS || p.noise_guard > ARCHES_MAX_BINS)
+    return set_err(ARCHES_E_CONFIG, "device path supports truncation and noise_guard <= %d",
+                   ARCHES_MAX_BINS);
+  if (p.mmse_block_prbs < 1) return set_err(ARCHES_E_CONFIG, "mmse_block_prbs must be >= 1");
+  if (p.n_mcs < 1 || p.n_mcs > ARCHES_MAX_MCS) return set_err(ARCHES_E_CONFIG, "n_mcs outside 1..%d", ARCHES_MAX_MCS);
+  if (p.window_length < 1 || p.dapp_window_slots < 1 || p.decision_period_slots < 1)
+    return set_err(ARCHES_E_CONFIG, "window lengths and periods must be positive");
+  if (p.assumed_delay_spread < 0) return set_err(ARCHES_E_CONFIG, "delay_spread must be >= 0");
+
+  arches_plan* P = new arches_plan();
+  memset(P, 0, sizeof(*P));
+  P->g = g;
+  P->p = p;
+  PlanDev& d = P->dev;
+  d.A = g.n_ant;
+  d.N = N;
+  d.M = M;
+  d.T = g.n_sym;
+  d.D = g.n_dmrs;
+  d.trunc = p.truncation;
+  d.guard = p.noise_guard;
+  int block = std::min(N, 12 * p.mmse_block_prbs);
+  if (N % block) block = N;  // expert_bank.py:166-168
+  d.block = block;
+  d.n_blocks = N / block;
+  const int pil_per_block = block / 2;
+  d.diag = (d.n_blocks == 1 && M >= 8) ? 1 : 0;
+  d.L = std::max(std::max(p.truncation, p.noise_guard), 8);
+  d.n_tiles = (N + ARCHES_TILE - 1) / ARCHES_TILE;
+  d.nbt_max = 1;
+  for (int t = 0; t < d.n_tiles; ++t) {
+    const int k0 = t * ARCHES_TILE, k1 = std::min(N, k0 + ARCHES_TILE) - 1;
+    d.nbt_max = std::max(d.nbt_max, std::min(d.n_blocks - 1, k1 / block) - k0 / block + 1);
+  }
+  for (int j = 0; j < g.n_dmrs; ++j) d.dsym[j] = g.dmrs_symbols[j];
+  time_interp(g, d);
+  d.ridge = p.ridge;
+  // pdp_powers (radio_scene.py:130-137), numpy pairwise order for 8 terms
+  double e[8];
+  if (p.assumed_delay_spread <= 0) {
+    for (int l = 0; l < 8; ++l) d.pdp[l] = l == 0 ? 1.0 : 0.0;
+  } else {
+    for (int l = 0; l < 8; ++l) e[l] = exp(-(double)l / p.assumed_delay_spread);
+    const double sum = ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
+    for (int l = 0; l < 8; ++l) d.pdp[l] = e[l] / sum;
+  }
+  for (int l = 0; l < ARCHES_MAX_BINS; ++l) {
+    const double ang = 2.0 * M_PI * (double)(l % N) / (double)N;
+    d.ai_fac[l] = make_double2((1.0 + cos(ang)) / N, sin(ang) / N);
+  }
+  // KPM / control
+  d.sinr_cap_db = p.sinr_cap_db;
+  d.lcid4_fraction = p.lcid4_fraction;
+  d.lcid4_jitter = p.lcid4_jitter;
+  d.crc_margin_db = p.crc_margin_db;
+  d.crc_scale_db = p.crc_scale_db;
+  d.slot_us = g.slot_duration_us;
+  {
+    volatile double us = g.slot_duration_us;
+    volatile double s = us * 1e-6;
+    d.slot_s = s;
+  }
+  d.slot_ns = (int64_t)llround(g.slot_duration_us * 1000.0);
+  d.n_prb = g.n_prb;
+  d.mac_header_bytes = p.mac_header_bytes;
+  d.window_length = p.window_length;
+  d.n_mcs = p.n_mcs;
+  for (int i = 0; i < p.n_mcs; ++i) {
+    d.mcs_thr[i] = p.mcs_threshold_db[i];
+    d.mcs_rate[i] = p.mcs_rate[i];
+    d.mcs_qam[i] = p.mcs_qam[i];
+  }
+  d.exec_mode = p.exec_mode;
+  d.policy = p.policy;
+  d.fixed_mode = p.fixed_mode;
+  d.decision_period = p.decision_period_slots;
+  d.dapp_window = p.dapp_window_slots;
+  d.decision_delay_ns = p.decision_delay_ns;
+  d.failsafe_timeout_ns = p.failsafe_timeout_ns;
+  d.crc_key = p.crc_purpose_key;
+
+  // ---- device tables
+  std::vector<float2> wM(M), wN(N), syn((size_t)d.L * ARCHES_TILE);
+  for (int j = 0; j < M; ++j) {
+    const double a = 2.0 * M_PI * (double)j / (double)M;
+    wM[j] = make_float2((float)cos(a), (float)sin(a));
+  }
+  for (int j = 0; j < N; ++j) {
+    const double a = 2.0 * M_PI * (double)j / (double)N;
+    wN[j] = make_float2((float)cos(a), (float)sin(a));
+  }
+  for (int l = 0; l < d.L; ++l)
+    for (int j = 0; j < ARCHES_TILE; ++j) {
+      const long long idx = ((long long)l * j) % N;
+      const double a = -2.0 * M_PI * (double)idx / (double)N;
+      syn[(size_t)l * ARCHES_TILE + j] = make_float2((float)cos(a), (float)sin(a));
+    }
+  std::vector<double2> gram(64);
+  for (int l = 0; l < 8; ++l)
+    for (int lp = 0; lp < 8; ++lp) {
+      double re = 0, im = 0;
+      for (int q = 0; q < pil_per_block; ++q) {
+        const long long idx = (((long long)(l - lp) * 2 * q) % N + N) % N;
+        const double a = 2.0 * M_PI * (double)idx / (double)N;
+        re += cos(a);
+        im += sin(a);
+      }
+      gram[l * 8 + lp] = make_double2(re, im);
+    }
+  const size_t off_wN = align256(M * sizeof(float2));
+  const size_t off_syn = off_wN + align256(N * sizeof(float2));
+  const size_t off_gram = off_syn + align256(syn.size() * sizeof(float2));
+  const size_t total = off_gram + align256(64 * sizeof(double2));
+  unsigned char* buf = nullptr;
+  cudaError_t err = cudaMalloc(&buf, total);
+  if (err != cudaSuccess) {
+    delete P;
+    return set_err(ARCHES_E_CUDA, "cudaMalloc(plan tables): %s", cudaGetErrorString(err));
+  }
+  cudaMemcpy(buf, wM.data(), M * sizeof(float2), cudaMemcpyHostToDevice);
+  cudaMemcpy(buf + off_wN, wN.data(), N * sizeof(float2), cudaMemcpyHostToDevice);
+  cudaMemcpy(buf + off_syn, syn.data(), syn.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  err = cudaMemcpy(buf + off_gram, gram.data(), 64 * sizeof(double2), cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) {
+    cudaFree(buf);
+    delete P;
+    return set_err(ARCHES_E_CUDA, "plan table upload: %s", cudaGetErrorString(err));
+  }
+  P->dev_tables = buf;
+  d.wM = reinterpret_cast<const float2*>(buf);
+  d.wN = reinterpret_cast<const float2*>(buf + off_wN);
+  d.syn = reinterpret_cast<const float2*>(buf + off_syn);
+  d.gram = reinterpret_cast<const double2*>(buf + off_gram);
+
+  // ---- K1 launch geometry
+  const int AD = d.A * d.D;
+  P->k1_per_chunk = (!d.diag && d.n_blocks > 1) ? 1 : 0;
+  int chunk = std::max(32, std::min(256, (8192 / AD) / 32 * 32));
+  if (P->k1_per_chunk) chunk = pil_per_block;
+  P->k1_chunk = chunk;
+  auto k1_smem = [&](int ch) {
+    const size_t stage = std::max((size_t)AD * ch, (size_t)ARCHES_K1_THREADS * ARCHES_RA * ARCHES_RL);
+    return stage * sizeof(float2) + (size_t)AD * d.L * sizeof(double2) + 64 * sizeof(double) +
+           64 * sizeof(double2);
+  };
+  P->k1_smem = k1_smem(chunk);
+  P->k1_full_chunk = std::max(32, std::min(256, (8192 / AD) / 32 * 32));
+  P->k1_full_smem = k1_smem(P->k1_full_chunk);
+  P->k2_smem = ((size_t)d.nbt_max * AD * 8 + (size_t)AD * d.trunc) * sizeof(float2);
+  *out = P;
+  return ARCHES_OK;
+}
+
+extern "C" int arches_plan_destroy(arches_plan* plan) {
+  if (!plan) return ARCHES_OK;
+  if (plan->dev_tables) cudaFree(plan->dev_tables);
+  delete plan;
+  return ARCHES_OK;
+}
+
+extern "C" int32_t arches_plan_bins(const arches_plan* plan) { return plan ? plan->dev.L : 0; }
+
+extern "C" size_t arches_state_bytes(const arches_plan* plan, int32_t n_streams) {
+  return (size_t)n_streams * state_stride_bytes(plan->dev.window_length, plan->dev.dapp_window);
+}
+
+extern "C" size_t arches_workspace_bytes(const arches_plan* plan, int32_t n_units) {
+  return ws_layout(plan, n_units).total;
+}
+
+extern "C" int arches_state_init(const arches_plan* plan, void* state, int32_t n_streams,
+                                 arches_stream_t stream) {
+  if (!plan || !state || n_streams < 1) return set_err(ARCHES_E_CONTRACT, "bad state_init args");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaMemsetAsync(state, 0, arches_state_bytes(plan, n_streams), s));
+  k4_state_init<<<(n_streams + 127) / 128, 128, 0, s>>>(plan->dev, state, n_streams);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+// ------------------------------------------------------------ K1
+template <class Src>
+static int launch_k1(const arches_plan* P, int n_units, const Src& src, const K1Out& o, int npts,
+                     int chunk, size_t smem, bool per_chunk, cudaStream_t s) {
+  if (per_chunk) {
+    auto kern = k1_analyze<Src, true>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<n_units, ARCHES_K1_THREADS, smem, s>>>(P->dev, src, o, npts, chunk);
+  } else {
+    auto kern = k1_analyze<Src, false>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<n_units, ARCHES_K1_THREADS, smem, s>>>(P->dev, src, o, npts, chunk);
+  }
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                                 const void* y, const void* pilots, double* sigma2_hat, void* ws,
+                                 arches_stream_t stream) {
+  if (!plan || !y || !pilots || !ws || n_streams < 1 || n_slots < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad ls_analyze args");
+  const int n_units = n_streams * n_slots;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const WsLayout w = ws_layout(plan, n_units);
+  GridCombSrc src{reinterpret_cast<const float2*>(y), reinterpret_cast<const float2*>(pilots), n_slots};
+  K1Out o{ws_at<double>(ws, w.sigma2), nullptr, ws_at<float2>(ws, w.coef),
+          plan->k1_per_chunk ? ws_at<double2>(ws, w.block_bins) : nullptr,
+          K1_NOISE | K1_MMSE | K1_AI};
+  int rc = launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem,
+                     plan->k1_per_chunk, s);
+  if (rc) return rc;
+  if (sigma2_hat)
+    CUDA_TRY(cudaMemcpyAsync(sigma2_hat, ws_at<double>(ws, w.sigma2), n_units * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
+  return ARCHES_OK;
+}
+
+// ------------------------------------------------------------ K2
+template <int NE>
+static int launch_k2(const arches_plan* P, int n_units, const K2Args& a, cudaStream_t s) {
+  const PlanDev& d = P->dev;
+  dim3 grid(d.n_tiles, n_units);
+  const size_t smem = P->k2_smem;
+  int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : d.A <= 4 ? 4 : d.A <= 8 ? 8 : 0;
+  if (!na) return set_err(ARCHES_E_CONFIG, "device equaliser path supports n_ant <= 8 (got %d)", d.A);
+#define K2_CASE(NA_, ND_)                                                                   \
+  if (na == NA_ && d.D == ND_) {                                                            \
+    auto kern = k2_synth_equalize<NA_, ND_, NE>;                                            \
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    kern<<<grid, ARCHES_TILE, smem, s>>>(d, a);                                             \
+    LAUNCH_CHECK();                                                                         \
+    return ARCHES_OK;                                                                       \
+  }
+  K2_CASE(1, 1) K2_CASE(1, 2) K2_CASE(1, 3) K2_CASE(1, 4)
+  K2_CASE(2, 1) K2_CASE(2, 2) K2_CASE(2, 3) K2_CASE(2, 4)
+  K2_CASE(4, 1) K2_CASE(4, 2) K2_CASE(4, 3) K2_CASE(4, 4)
+  K2_CASE(8, 1) K2_CASE(8, 2) K2_CASE(8, 3) K2_CASE(8, 4)
+#undef K2_CASE
+  return set_err(ARCHES_E_CONFIG, "unsupported (n_ant, n_dmrs) = (%d, %d)", d.A, d.D);
+}
+
+extern "C" int arches_experts_equalize(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                                       const void* y, const void* tx, const double* noise_var,
+                                       const uint64_t* seeds, int64_t first_slot, void* h_mmse,
+                                       void* h_ai, arches_telemetry* tel, void* ws,
+                                       arches_stream_t stream) {
+  if (!plan || !y || !tx || !noise_var || !seeds || !ws || !tel || n_streams < 1 || n_slots < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad experts_equalize args");
+  if (first_slot < 0) return set_err(ARCHES_E_CONTRACT, "slot_index must be >= 0");
+  const int n_units = n_streams * n_slots;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const WsLayout w = ws_layout(plan, n_units);
+  CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.counters), 0, n_units * sizeof(unsigned int), s));
+  K2Args a;
+  memset(&a, 0, sizeof(a));
+  a.y = reinterpret_cast<const float2*>(y);
+  a.tx = reinterpret_cast<const float2*>(tx);
+  a.coef = ws_at<float2>(ws, w.coef);
+  a.nv = noise_var;
+  a.sigma2 = ws_at<double>(ws, w.sigma2);
+  a.seeds = seeds;
+  a.h_mmse = reinterpret_cast<float2*>(h_mmse);
+  a.h_ai = reinterpret_cast<float2*>(h_ai);
+  a.parts = ws_at<TilePartial>(ws, w.parts);
+  a.counters = ws_at<unsigned int>(ws, w.counters);
+  a.tel = tel;
+  a.first_slot = first_slot;
+  a.n_slots = n_slots;
+  return launch_k2<2>(plan, n_units, a, s);
+}
+
+// ------------------------------------------------------------ K4 / K5
+extern "C" int arches_kpm_scan(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                               const arches_telemetry* tel, const int8_t* regime,
+                               const arches_tree* tree, void* state, arches_kpm* kpm,
+                               arches_message* msg_log, int32_t* msg_count, int32_t msg_cap,
+                               arches_stream_t stream) {
+  if (!plan || !tel || !state || !kpm || n_streams < 1 || n_slots < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad kpm_scan args");
+  if (plan->dev.policy == ARCHES_POLICY_TREE && !tree)
+    return set_err(ARCHES_E_CONTRACT, "tree policy needs a tree");
+  if (plan->dev.policy == ARCHES_POLICY_ORACLE && !regime)
+    return set_err(ARCHES_E_CONTRACT, "oracle policy needs the regime timeline");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  K4Args a{tel, regime, tree, state, kpm, msg_log, msg_count, msg_cap, n_streams, n_slots};
+  k4_kpm_scan<<<(n_streams + 31) / 32, 32, 0, s>>>(plan->dev, a);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                                int64_t first_slot, const void* y, const void* tx,
+                                const void* pilots, const double* noise_var, const uint64_t* seeds,
+                                const int8_t* regime, const arches_tree* tree, void* state,
+                                void* h_mmse, void* h_ai, arches_telemetry* tel, arches_kpm* kpm,
+                                arches_message* msg_log, int32_t* msg_count, int32_t msg_cap,
+                                void* ws, arches_stream_t stream) {
+  int rc = arches_ls_analyze(plan, n_streams, n_slots, y, pilots, nullptr, ws, stream);
+  if (rc) return rc;
+  rc = arches_experts_equalize(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
+                               h_mmse, h_ai, tel, ws, stream);
+  if (rc) return rc;
+  return arches_kpm_scan(plan, n_streams, n_slots, tel, regime, tree, state, kpm, msg_log,
+                         msg_count, msg_cap, stream);
+}
+
+extern "C" int arches_switch_copy(const arches_plan* plan, int32_t n_units, const arches_kpm* kpm,
+                                  const void* h_mmse, void* h_ai, arches_stream_t stream) {
+  if (!plan || !kpm || !h_mmse || !h_ai || n_units < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad switch_copy args");
+  const size_t per_unit = (size_t)plan->dev.A * plan->dev.D * plan->dev.N;  // complex values
+  if (per_unit % 2) return set_err(ARCHES_E_CONTRACT, "unit size must be even");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t f4 = per_unit / 2;
+  dim3 grid((unsigned)std::min<size_t>((f4 + 255) / 256, 64), n_units);
+  k5_switch_copy<<<grid, 256, 0, s>>>(kpm, reinterpret_cast<const float4*>(h_mmse),
+                                      reinterpret_cast<float4*>(h_ai), f4, n_units);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_switch_copy_one(const int32_t* mode, const void* src, void* dst, size_t n,
+                                      arches_stream_t stream) {
+  if (!mode || !src || !dst) return set_err(ARCHES_E_CONTRACT, "bad switch_copy_one args");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned blocks = (unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 1184));
+  k5_switch_copy_one<<<blocks, 256, 0, s>>>(mode, reinterpret_cast<const float2*>(src),
+                                            reinterpret_cast<float2*>(dst), n);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+// ------------------------------------------------------------ compat forms
+extern "C" int arches_ls_materialize(const arches_plan* plan, int32_t n_units, const void* y,
+                                     const void* pilots, void* ls, arches_stream_t stream) {
+  if (!plan || !y || !pilots || !ls || n_units < 1) return set_err(ARCHES_E_CONTRACT, "bad ls args");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  GridCombSrc src{reinterpret_cast<const float2*>(y), reinterpret_cast<const float2*>(pilots), 1};
+  k_ls_materialize<<<592, 256, 0, s>>>(plan->dev, src, reinterpret_cast<float2*>(ls), n_units);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_expert_from_ls(const arches_plan* plan, int32_t n_units, int32_t which,
+                                     const void* ls, const double* noise_var_in, double* sigma2_hat,
+                                     void* out, void* ws, arches_stream_t stream) {
+  if (!plan || !ls || !ws || n_units < 1 || which < 0 || which > 2)
+    return set_err(ARCHES_E_CONTRACT, "bad expert_from_ls args");
+  if ((which == 1 || which == 2) && !out) return set_err(ARCHES_E_CONTRACT, "missing output");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const WsLayout w = ws_layout(plan, n_units);
+  const float2* l = reinterpret_cast<const float2*>(ls);
+  int rc;
+  if (which == 2) {
+    LsFullSrc src{l};
+    K1Out o{nullptr, nullptr, ws_at<float2>(ws, w.coef), nullptr, K1_AI};
+    rc = launch_k1(plan, n_units, src, o, plan->dev.N, plan->k1_full_chunk, plan->k1_full_smem,
+                   false, s);
+  } else {
+    LsCombSrc src{l};
+    K1Out o{sigma2_hat ? sigma2_hat : ws_at<double>(ws, w.sigma2), noise_var_in,
+            which == 1 ? ws_at<float2>(ws, w.coef) : nullptr,
+            plan->k1_per_chunk ? ws_at<double2>(ws, w.block_bins) : nullptr,
+            which == 1 ? (K1_NOISE | K1_MMSE) : K1_NOISE};
+    rc = launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem,
+                   plan->k1_per_chunk, s);
+  }
+  if (rc || which == 0) return rc;
+  dim3 grid((plan->dev.N + 127) / 128, n_units);
+  k_synth_one<<<grid, 128, 0, s>>>(plan->dev, ws_at<float2>(ws, w.coef), which,
+                                   reinterpret_cast<float2*>(out));
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_equalize(const arches_plan* plan, int32_t n_units, const void* y,
+                               const void* est, const void* tx, const double* noise_var,
+                               double* sinr_db, double* abs_mean, double* rsrp, void* x_hat,
+                               void* ws, arches_stream_t stream) {
+  if (!plan || !y || !est || !tx || !noise_var || !ws || n_units < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad equalize args");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const WsLayout w = ws_layout(plan, n_units);
+  CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.counters), 0, n_units * sizeof(unsigned int), s));
+  K2Args a;
+  memset(&a, 0, sizeof(a));
+  a.y = reinterpret_cast<const float2*>(y);
+  a.tx = reinterpret_cast<const float2*>(tx);
+  a.est = reinterpret_cast<const float2*>(est);
+  a.nv = noise_var;
+  a.x_hat = reinterpret_cast<float2*>(x_hat);
+  a.parts = ws_at<TilePartial>(ws, w.parts);
+  a.counters = ws_at<unsigned int>(ws, w.counters);
+  a.sinr_out = sinr_db;
+  a.abs_out = abs_mean;
+  a.rsrp_out = rsrp;
+  a.n_slots = 1;
+  return launch_k2<1>(plan, n_units, a, s);
+}
+
+extern "C" int arches_window_features(const double* rows, int32_t n_rows, double* out,
+                                      arches_stream_t stream) {
+  if (!rows || !out) return set_err(ARCHES_E_CONTRACT, "bad window_features args");
+  if (n_rows < 1) return set_err(ARCHES_E_CONTRACT, "empty KPM window");
+  k_window_features<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(rows, n_rows, out);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_tree_predict(const arches_tree* tree, const double* x, int32_t n,
+                                   int32_t n_features, int32_t* labels, arches_stream_t stream) {
+  if (!tree || !x || !labels || n < 1) return set_err(ARCHES_E_CONTRACT, "bad predict args");
+  k_tree_predict<<<(n + 127) / 128, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      tree, x, n, n_features, labels);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+// ------------------------------------------------------------ host helpers
+extern "C" const char* arches_last_error(void) { return g_err; }
+extern "C" const char* arches_version(void) { return ARCHES_VERSION; }
+
+extern "C" double arches_host_crc_uniform(uint64_t seed, uint64_t purpose_key, uint64_t slot) {
+  return arches_rng::stream_first_uniform(seed, purpose_key, slot);
+}
+
+extern "C" double arches_host_lcid4_jitter(uint64_t slot) { return arches_rng::lcid4_jitter(slot); }
+
+extern "C" uint64_t arches_host_blake2b64(const void* data, size_t len) {
+  if (len > 128) return 0;
+  return arches_rng::blake2b64(reinterpret_cast<const uint8_t*>(data), (int)len);
+}
+
+extern "C" int32_t arches_device_available(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n > 0 ? 1 : 0;
+}

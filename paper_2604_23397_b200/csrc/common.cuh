@@ -1,0 +1,115 @@
+// Shared device-side definitions of the ARCHES B200 hot path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/arches.h"
+
+#define ARCHES_TILE 128        // K2 subcarriers per CTA (one per thread)
+#define ARCHES_K1_THREADS 256  // K1 CTA size
+#define ARCHES_RA 4            // K1 register tile: (a,d) rows per thread
+#define ARCHES_RL 5            // K1 register tile: delay bins per thread
+#define ARCHES_MAX_AD (ARCHES_MAX_ANT * ARCHES_MAX_DMRS)
+#define ARCHES_FEATURES 10
+
+// Plan constants passed by value to every kernel (tables live in device memory).
+struct PlanDev {
+  int A, N, M, T, D, L;         // antennas, subcarriers, comb, symbols, dmrs, analysis bins
+  int trunc, guard;             // denoiser taps, noise guard
+  int n_blocks, block, diag;    // MMSE blocks, subcarriers per block, closed-form weights
+  int n_tiles;                  // K2 tiles per unit
+  int nbt_max;                  // max MMSE blocks overlapping one K2 tile
+  int dsym[ARCHES_MAX_DMRS];    // DMRS symbol indices
+  int is_dmrs[ARCHES_MAX_SYM];  // symbol -> dmrs slot or -1
+  int tw_d0[ARCHES_MAX_SYM], tw_d1[ARCHES_MAX_SYM];  // time interpolation taps
+  float tw_w0[ARCHES_MAX_SYM], tw_w1[ARCHES_MAX_SYM];
+  double ridge;
+  double pdp[8];                // MMSE prior powers p_l
+  float tw[ARCHES_MAX_SYM][ARCHES_MAX_DMRS];  // _time_interp_weights (phy_pipeline.py:227-242)
+  double2 ai_fac[ARCHES_MAX_BINS];  // (1 + e^{2 pi i l/N}) / N
+  const float2* wM;             // [M] e^{+2 pi i j / M}
+  const float2* wN;             // [N] e^{+2 pi i j / N}
+  const float2* syn;            // [L][TILE] e^{-2 pi i l j / N}
+  const double2* gram;          // [8][8] F^H F of one MMSE block
+  // KPM layer
+  double sinr_cap_db, lcid4_fraction, lcid4_jitter, crc_margin_db, crc_scale_db;
+  double slot_us, slot_s;
+  int64_t slot_ns;
+  int n_prb, mac_header_bytes, window_length, n_mcs;
+  double mcs_thr[ARCHES_MAX_MCS];
+  double mcs_rate[ARCHES_MAX_MCS];
+  int mcs_qam[ARCHES_MAX_MCS];
+  // control plane
+  int exec_mode, policy, fixed_mode, decision_period, dapp_window;
+  int64_t decision_delay_ns, failsafe_timeout_ns;
+  uint64_t crc_key;
+};
+
+// Per-unit coefficient record written by K1, read by K2 (workspace).
+//   cm[ad][b][8]  MMSE synthesis taps per block (float2)
+//   ca[ad][T]     AI synthesis taps (float2)
+__host__ __device__ inline size_t coef_floats2(const PlanDev& P) {
+  return (size_t)P.A * P.D * (P.n_blocks * 8 + P.trunc);
+}
+
+// K2 per-tile partial sums (fp64), reduced in tile order by the last CTA.
+struct TilePartial {
+  double abs_sum[2];
+  double pow_sum[2];
+  double sxx;
+  double sxy_re[2];
+  double sxy_im[2];
+  double syy[2];
+  double pad;
+};
+
+// Per-stream control state header (followed by rings, see state_layout).
+struct PendingMsg {
+  int64_t at_ns;
+  int32_t mode;
+  int32_t trigger;
+};
+
+struct StreamState {
+  int64_t next_slot;
+  int64_t cum_phy_bytes;
+  int64_t mac_total, l4_total;
+  int64_t last_delivery_ns;
+  int32_t mode, ndi;
+  int32_t win_fill, win_head;
+  int32_t n_pending, n_forced;
+  int32_t since_decision, feat_fill, feat_head, tripped;
+  int32_t last_msg_mode, pad;
+  PendingMsg pending[ARCHES_MAX_PENDING];
+  PendingMsg forced[ARCHES_MAX_PENDING];
+};
+
+__host__ __device__ inline size_t state_stride_bytes(int window, int dapp_window) {
+  size_t b = sizeof(StreamState) + (size_t)2 * window * sizeof(int32_t) +
+             (size_t)dapp_window * ARCHES_FEATURES * sizeof(double);
+  return (b + 255) & ~(size_t)255;
+}
+
+// ---------------------------------------------------------------- complex
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // conj(a) * b
+  return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ void cfma(float2& acc, float2 a, float2 b) {  // acc += a*b
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(a.y, b.x, acc.y);
+}
+__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}

@@ -1,0 +1,284 @@
+// K1 -- LS front end + delay-domain analysis (one CTA per unit).
+//
+// Replaces ls_estimate (expert_bank.py:96-116), estimate_noise_var (:199-214)
+// and the noise-dependent half of mmse_estimate/_wiener_matrix (:139-177) and
+// denoiser_estimate (:182-196).
+//
+// Exact factorisation used (derived in DESIGN.md s3):
+//   bins   B[ad][l]  = sum_m h[ad][m] e^{+2 pi i l m / M}          (l < L)
+//   sigma2 = (sum |h|^2 - sum_{ad, l<guard} |B|^2 / M) / (AD (M - guard))   (Parseval)
+//   MMSE   out[k] = sum_{l<8} c_l e^{-2 pi i l k / N},  c = P (Gamma P + s I)^-1 B
+//          (Gamma = M I for one block with M >= 8 -> c_l = p_l B_l / (M p_l + s))
+//   AI     out[k] = sum_{l<T} c_l e^{-2 pi i l k / N},  c_l = (1 + e^{2 pi i l/N}) B_l / N
+// The analysis is a (AD x npts) x (npts x L) complex contraction; each thread
+// owns a 4 (ad) x 5 (l) register tile over a K-slice of points, twiddles come
+// from an exactly rounded table plus a <= 4-step recurrence.
+#pragma once
+#include "common.cuh"
+
+// --- point sources -------------------------------------------------------
+// pipeline: comb REs of the received grid divided by the pilots
+struct GridCombSrc {
+  const float2* y;    // [u][A][T][N]
+  const float2* pil;  // [stream][M][D]
+  int n_slots;
+  static constexpr bool kComb = true;
+  __device__ __forceinline__ float2 load(const PlanDev& P, int u, int ad, int m) const {
+    const int a = ad / P.D, d = ad - a * P.D;
+    const float2 v = __ldg(&y[(((size_t)u * P.A + a) * P.T + P.dsym[d]) * P.N + 2 * m]);
+    const float2 p = __ldg(&pil[((size_t)(u / n_slots) * P.M + m) * P.D + d]);
+    const float inv = 1.0f / (p.x * p.x + p.y * p.y);
+    const float2 q = cmulc(p, v);  // conj(p) * v
+    return make_float2(q.x * inv, q.y * inv);
+  }
+};
+// compat: comb positions of a materialised LS grid ls[u][A][D][N]
+struct LsCombSrc {
+  const float2* ls;
+  static constexpr bool kComb = true;
+  __device__ __forceinline__ float2 load(const PlanDev& P, int u, int ad, int m) const {
+    return __ldg(&ls[((size_t)u * P.A * P.D + ad) * P.N + 2 * m]);
+  }
+};
+// compat: every subcarrier of an LS grid (general denoiser input)
+struct LsFullSrc {
+  const float2* ls;
+  static constexpr bool kComb = false;
+  __device__ __forceinline__ float2 load(const PlanDev& P, int u, int ad, int k) const {
+    return __ldg(&ls[((size_t)u * P.A * P.D + ad) * P.N + k]);
+  }
+};
+
+// what K1 produces
+enum { K1_NOISE = 1, K1_MMSE = 2, K1_AI = 4 };
+
+struct K1Out {
+  double* sigma2;           // [u] (may be null)
+  const double* nv_in;      // [u] override (>= 0) or null
+  float2* coef;             // [u][coef_floats2]
+  double2* block_bins;      // [u][n_blocks][AD][8] scratch (per-chunk mode)
+  int what;
+};
+
+__device__ inline void solve8_gram(const PlanDev& P, double s, double2* K /*[8][8]*/) {
+  // K = Pd (Gamma Pd + s I)^-1, Gaussian elimination with partial pivoting on
+  // X^T: rows of K are solutions of (Gamma Pd + s I)^T z = Pd_row.
+  double2 a[8][16];
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      // (Gamma Pd + sI)^T [i][j] = (Gamma Pd + sI)[j][i] = Gamma[j][i] p_i + s delta
+      double2 g = P.gram[j * 8 + i];
+      a[i][j] = make_double2(g.x * P.pdp[i] + (i == j ? s : 0.0), g.y * P.pdp[i]);
+      a[i][8 + j] = make_double2(i == j ? P.pdp[i] : 0.0, 0.0);
+    }
+  for (int c = 0; c < 8; ++c) {
+    int piv = c;
+    double best = a[c][c].x * a[c][c].x + a[c][c].y * a[c][c].y;
+    for (int r = c + 1; r < 8; ++r) {
+      double v = a[r][c].x * a[r][c].x + a[r][c].y * a[r][c].y;
+      if (v > best) best = v, piv = r;
+    }
+    if (piv != c)
+      for (int j = 0; j < 16; ++j) {
+        double2 t = a[c][j];
+        a[c][j] = a[piv][j];
+        a[piv][j] = t;
+      }
+    const double den = a[c][c].x * a[c][c].x + a[c][c].y * a[c][c].y;
+    const double2 inv = make_double2(a[c][c].x / den, -a[c][c].y / den);
+    for (int j = 0; j < 16; ++j) a[c][j] = zmul(a[c][j], inv);
+    for (int r = 0; r < 8; ++r) {
+      if (r == c) continue;
+      const double2 f = a[r][c];
+      for (int j = 0; j < 16; ++j) {
+        const double2 t = zmul(f, a[c][j]);
+        a[r][j].x -= t.x;
+        a[r][j].y -= t.y;
+      }
+    }
+  }
+  // solution Z = X^{-T} Pd  =>  K = Z^T
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) K[j * 8 + i] = a[i][8 + j];
+}
+
+template <class Src, bool kPerChunk>
+__global__ void __launch_bounds__(ARCHES_K1_THREADS)
+    k1_analyze(const PlanDev P, const Src src, const K1Out out, const int npts, const int chunk) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int u = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int AD = P.A * P.D;
+  const int L = P.L;
+  const int n_ad_t = (AD + ARCHES_RA - 1) / ARCHES_RA;
+  const int n_l_t = (L + ARCHES_RL - 1) / ARCHES_RL;
+  const int n_tiles = n_ad_t * n_l_t;
+  const int KS = max(1, ARCHES_K1_THREADS / n_tiles);
+  const int tile = tid / KS, ks = tid - tile * KS;
+  const bool active = tile < n_tiles;
+  const int ad0 = (tile / n_l_t) * ARCHES_RA, l0 = (tile % n_l_t) * ARCHES_RL;
+  const float2* wtab = Src::kComb ? P.wM : P.wN;
+
+  // smem carve: [hs: AD*chunk float2 | red: 256*RA*RL float2 (aliased)]
+  //             [bins: AD*L double2] [scratch doubles 64] [K 64 double2]
+  float2* hs = reinterpret_cast<float2*>(smem_raw);
+  float2* red = hs;
+  const size_t stage = max((size_t)AD * chunk, (size_t)ARCHES_K1_THREADS * ARCHES_RA * ARCHES_RL);
+  double2* bins = reinterpret_cast<double2*>(hs + stage);
+  double* scr = reinterpret_cast<double*>(bins + (size_t)AD * L);
+  double2* Kmat = reinterpret_cast<double2*>(scr + 64);
+
+  for (int i = tid; i < AD * L; i += blockDim.x) bins[i] = make_double2(0.0, 0.0);
+
+  float2 acc[ARCHES_RA][ARCHES_RL];
+#pragma unroll
+  for (int i = 0; i < ARCHES_RA; ++i)
+#pragma unroll
+    for (int j = 0; j < ARCHES_RL; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  double energy = 0.0;
+
+  const int n_chunks = (npts + chunk - 1) / chunk;
+  for (int c = 0; c < n_chunks; ++c) {
+    const int base = c * chunk;
+    const int len = min(chunk, npts - base);
+    __syncthreads();  // hs reuse
+    float e32 = 0.f;
+    for (int e = tid; e < AD * chunk; e += blockDim.x) {
+      const int ad = e / chunk, j = e - ad * chunk;
+      float2 v = make_float2(0.f, 0.f);
+      if (j < len) v = src.load(P, u, ad, base + j);
+      hs[e] = v;
+      e32 = fmaf(v.x, v.x, fmaf(v.y, v.y, e32));
+    }
+    energy += (double)e32;
+    __syncthreads();
+    if (active) {
+      for (int j = ks; j < len; j += KS) {
+        const int pt = base + j;
+        const float2 w1 = __ldg(&wtab[pt]);
+        float2 w = __ldg(&wtab[(int)(((long long)l0 * pt) % npts)]);
+        float2 hv[ARCHES_RA];
+#pragma unroll
+        for (int i = 0; i < ARCHES_RA; ++i)
+          hv[i] = (ad0 + i < AD) ? hs[(ad0 + i) * chunk + j] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int l = 0; l < ARCHES_RL; ++l) {
+#pragma unroll
+          for (int i = 0; i < ARCHES_RA; ++i) cfma(acc[i][l], hv[i], w);
+          w = cmul(w, w1);
+        }
+      }
+    }
+    if (kPerChunk || c == n_chunks - 1) {
+      // reduce the K-slices of this chunk (or of everything) in fixed order, fp64
+      __syncthreads();  // red aliases hs
+#pragma unroll
+      for (int i = 0; i < ARCHES_RA; ++i)
+#pragma unroll
+        for (int l = 0; l < ARCHES_RL; ++l) {
+          red[(size_t)tid * ARCHES_RA * ARCHES_RL + i * ARCHES_RL + l] = acc[i][l];
+          if (kPerChunk) acc[i][l] = make_float2(0.f, 0.f);
+        }
+      __syncthreads();
+      for (int o = tid; o < AD * L; o += blockDim.x) {
+        const int ad = o / L, l = o - ad * L;
+        const int t = (ad / ARCHES_RA) * n_l_t + l / ARCHES_RL;
+        const int slot = (ad % ARCHES_RA) * ARCHES_RL + (l % ARCHES_RL);
+        double sx = 0.0, sy = 0.0;
+        for (int k = 0; k < KS; ++k) {
+          const float2 v = red[(size_t)(t * KS + k) * ARCHES_RA * ARCHES_RL + slot];
+          sx += (double)v.x;
+          sy += (double)v.y;
+        }
+        bins[o].x += sx;
+        bins[o].y += sy;
+        if (kPerChunk && l < 8 && out.block_bins) {
+          // block-local bins: remove the phase of the block origin (m0 = base)
+          double sn, cs;
+          sincospi(-2.0 * (double)(((long long)l * base) % npts) / (double)npts, &sn, &cs);
+          out.block_bins[(((size_t)u * P.n_blocks + c) * AD + ad) * 8 + l] =
+              make_double2(sx * cs - sy * sn, sx * sn + sy * cs);
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- energy reduction (fixed order)
+  energy = warp_sum(energy);
+  if ((tid & 31) == 0) scr[tid >> 5] = energy;
+  __syncthreads();
+  if (tid == 0) {
+    double e = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) e += scr[w];
+    double sg = 0.0;
+    if (Src::kComb) {
+      for (int ad = 0; ad < AD; ++ad)
+        for (int l = 0; l < P.guard; ++l) {
+          const double2 b = bins[ad * L + l];
+          sg += b.x * b.x + b.y * b.y;
+        }
+    }
+    const double nvhat = Src::kComb ? (e - sg / (double)P.M) / ((double)AD * (P.M - P.guard)) : 0.0;
+    if (out.sigma2) out.sigma2[u] = nvhat;
+    double s = nvhat;
+    if (out.nv_in && out.nv_in[u] >= 0.0) s = out.nv_in[u];
+    scr[32] = s + P.ridge;
+    if ((out.what & K1_MMSE) && !P.diag) solve8_gram(P, s + P.ridge, Kmat);
+  }
+  __syncthreads();
+  if (!out.coef) return;
+  const double s = scr[32];
+  float2* cm = out.coef + (size_t)u * coef_floats2(P);
+  float2* ca = cm + (size_t)AD * P.n_blocks * 8;
+  if (out.what & K1_MMSE) {
+    if (P.diag) {
+      for (int o = tid; o < AD * 8; o += blockDim.x) {
+        const int ad = o >> 3, l = o & 7;
+        const double w = P.pdp[l] / ((double)P.M * P.pdp[l] + s);
+        const double2 b = bins[ad * L + l];
+        cm[o] = make_float2((float)(w * b.x), (float)(w * b.y));
+      }
+    } else {
+      const int nb = P.n_blocks;
+      for (int o = tid; o < AD * nb * 8; o += blockDim.x) {
+        const int ad = o / (nb * 8), r = o - ad * nb * 8, b = r >> 3, l = r & 7;
+        double2 acc2 = make_double2(0.0, 0.0);
+        for (int lp = 0; lp < 8; ++lp) {
+          const double2 bb = (nb == 1) ? bins[ad * L + lp]
+                                       : out.block_bins[(((size_t)u * nb + b) * AD + ad) * 8 + lp];
+          const double2 t = zmul(Kmat[l * 8 + lp], bb);
+          acc2.x += t.x;
+          acc2.y += t.y;
+        }
+        cm[o] = make_float2((float)acc2.x, (float)acc2.y);
+      }
+    }
+  }
+  if (out.what & K1_AI) {
+    for (int o = tid; o < AD * P.trunc; o += blockDim.x) {
+      const int ad = o / P.trunc, l = o - ad * P.trunc;
+      const double2 b = bins[ad * L + l];
+      double2 v;
+      if (Src::kComb) {
+        v = zmul(P.ai_fac[l], b);
+      } else {
+        v = make_double2(b.x / (double)P.N, b.y / (double)P.N);
+      }
+      ca[o] = make_float2((float)v.x, (float)v.y);
+    }
+  }
+}
+
+// ls_estimate materialised: ls[u][A][D][N], odd subcarriers copy the even one
+__global__ void k_ls_materialize(const PlanDev P, const GridCombSrc src, float2* ls, int n_units) {
+  const size_t total = (size_t)n_units * P.A * P.D * P.N;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % P.N);
+    const size_t r = i / P.N;
+    const int ad = (int)(r % (P.A * P.D));
+    const int u = (int)(r / (P.A * P.D));
+    ls[i] = src.load(P, u, ad, k >> 1);
+  }
+}

@@ -1,0 +1,324 @@
+// K2 -- expert synthesis + switch telemetry + equaliser (one CTA per 128
+// subcarriers of one unit, one thread per subcarrier).
+//
+// Replaces the synthesis halves of mmse_estimate (expert_bank.py:170-175) and
+// denoiser_estimate (:192-194), the |H| / |H|^2 telemetry of run_slot
+// (phy_pipeline.py:453-455) and equalize (:253-279), for both experts in a
+// single pass over y and tx.  The last CTA of each unit reduces the per-tile
+// fp64 partials in tile order (deterministic) and derives both candidates'
+// link-adaptation / CRC / MAC quantities (phy_pipeline.py:192-222,462-470).
+#pragma once
+#include "common.cuh"
+#include "rng.cuh"
+
+// ------------------------------------------------------- exact fp64 helpers
+// (no FMA contraction: the KPM arithmetic must round like CPython)
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// SINR of equalize() from one-pass sums (phy_pipeline.py:268-279)
+__device__ inline double sinr_from_sums(double sxx, double sre, double sim, double syy,
+                                        double cap) {
+  const double s2 = sre * sre + sim * sim;
+  const double err_p = syy - s2 / sxx;
+  if (!(err_p > 0.0)) return cap;
+  const double ar = sre / sxx, ai = sim / sxx;
+  const double v = 10.0 * log10((ar * ar + ai * ai) * sxx / err_p);
+  return v < cap ? v : cap;
+}
+
+// link_adapt / transport_block / crc_outcome / MAC split of one candidate
+__device__ inline void kpm_candidate(const PlanDev& P, double sinr, double u_crc, double frac,
+                                     int& mcs, int& tb, int& ncb, int& crc, int& mac_rx,
+                                     int& l4_rx) {
+  int cnt = 0;
+  for (int i = 0; i < P.n_mcs; ++i) cnt += (P.mcs_thr[i] <= sinr) ? 1 : 0;
+  if (sinr != sinr) cnt = P.n_mcs;  // numpy sorts NaN last
+  mcs = max(cnt - 1, 0);
+  const long long prod = (long long)P.n_prb * 12 * 11 * P.mcs_qam[mcs];
+  tb = (int)floor(xmul((double)prod, P.mcs_rate[mcs]) / 8.0);
+  ncb = max(1, (int)ceil(xdiv((double)((long long)tb * 8), 8448.0)));
+  const double centre = xsub(P.mcs_thr[mcs], P.crc_margin_db);
+  const double z = xdiv(-xsub(sinr, centre), P.crc_scale_db);
+  const double p = xdiv(1.0, xadd(1.0, exp(z)));
+  crc = (u_crc < p) ? 1 : 0;
+  const int pdu = max(tb - P.mac_header_bytes, 0);
+  mac_rx = crc ? pdu : 0;
+  l4_rx = (int)trunc(xmul((double)mac_rx, frac));
+}
+
+__device__ inline double lcid4_frac(const PlanDev& P, long long slot) {
+  const double j = arches_rng::lcid4_jitter((uint64_t)slot);
+  const double f = xadd(P.lcid4_fraction, xmul(P.lcid4_jitter, j));
+  return fmin(fmax(f, 0.0), 1.0);
+}
+
+// last-CTA finalisation: reduce partials (tile order) and fill the telemetry
+__device__ inline void finalize_unit(const PlanDev& P, const TilePartial* parts, int n_tiles,
+                                     const double* sigma2, uint64_t seed, long long slot,
+                                     int n_experts, arches_telemetry* tel) {
+  double acc[11];
+  for (int i = 0; i < 11; ++i) acc[i] = 0.0;
+  for (int t = 0; t < n_tiles; ++t) {
+    const double* p = reinterpret_cast<const double*>(&parts[t]);
+    for (int i = 0; i < 11; ++i) acc[i] += p[i];
+  }
+  const double cnt = (double)P.A * P.D * P.N;
+  arches_telemetry out;
+  out.sigma2_hat = sigma2 ? *sigma2 : 0.0;
+  const double u_crc = arches_rng::stream_first_uniform(seed, P.crc_key, (uint64_t)slot);
+  const double frac = lcid4_frac(P, slot);
+  for (int e = 0; e < 2; ++e) {
+    const int src = (n_experts == 2) ? e : 0;
+    out.abs_mean[e] = acc[0 + src] / cnt;
+    out.rsrp[e] = acc[2 + src] / cnt;
+    out.sinr_db[e] = sinr_from_sums(acc[4], acc[5 + src], acc[7 + src], acc[9 + src], P.sinr_cap_db);
+    kpm_candidate(P, out.sinr_db[e], u_crc, frac, out.mcs[e], out.tb_bytes[e], out.num_cb[e],
+                  out.crc[e], out.mac_rx[e], out.lcid4_rx[e]);
+  }
+  *tel = out;
+}
+
+// block reduction of the per-thread partials into this tile's TilePartial
+__device__ inline void reduce_tile(double (&v)[11], double* scr /*[11][warps]*/,
+                                   TilePartial* dst) {
+  const int warps = blockDim.x >> 5, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 11; ++i) {
+    const double s = warp_sum(v[i]);
+    if ((threadIdx.x & 31) == 0) scr[i * warps + w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 11) {
+    double s = 0.0;
+    for (int j = 0; j < warps; ++j) s += scr[threadIdx.x * warps + j];
+    reinterpret_cast<double*>(dst)[threadIdx.x] = s;
+  }
+}
+
+// arrive on the unit counter; returns true in the last CTA (all threads)
+__device__ inline bool last_block_arrive(unsigned int* counter, int expected, int* flag) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(counter, 1u);
+    const bool last = (prev == (unsigned int)expected - 1);
+    if (last) *counter = 0u;  // re-arm for the next launch / graph replay
+    *flag = last;
+  }
+  __syncthreads();
+  const bool last = *flag;
+  if (last) __threadfence();
+  return last;
+}
+
+struct K2Args {
+  const float2* y;        // [u][A][T][N]
+  const float2* tx;       // [u][T][N]
+  const float2* coef;     // [u][coef]   (synthesis) or null
+  const float2* est;      // [u][A][D][N] given estimate (compat equalize) or null
+  const double* nv;       // [u] true noise variance
+  const double* sigma2;   // [u] sigma2_hat (telemetry passthrough) or null
+  const uint64_t* seeds;  // [stream]
+  float2* h_mmse;         // outputs (may be null)
+  float2* h_ai;
+  float2* x_hat;          // [u][T][N] compat only
+  TilePartial* parts;     // [u][n_tiles]
+  unsigned int* counters; // [u]
+  arches_telemetry* tel;  // [u]
+  double* sinr_out;       // compat: [u] sinr / abs_mean / rsrp of expert 0
+  double* abs_out;
+  double* rsrp_out;
+  long long first_slot;
+  int n_slots;
+};
+
+// NE experts held per thread: 2 = pipeline (MMSE, AI synthesised),
+// 1 = compat (estimate loaded from args.est)
+template <int NA, int ND, int NE>
+__global__ void __launch_bounds__(ARCHES_TILE)
+    k2_synth_equalize(const PlanDev P, const K2Args args) {
+  // dynamic smem: [s_cm: nbt_max][AD*8] rotated MMSE taps, [s_ca: AD*trunc] rotated AI taps
+  extern __shared__ __align__(16) float2 s_dyn[];
+  __shared__ double s_scr[11 * (ARCHES_TILE / 32)];
+  __shared__ int s_flag;
+  const int u = blockIdx.y;
+  const int tile = blockIdx.x;
+  const int k0 = tile * ARCHES_TILE;
+  const int j = threadIdx.x;
+  const int k = k0 + j;
+  const bool valid = k < P.N;
+  const int AD = P.A * ND;  // runtime antennas (<= NA, padded lanes masked)
+  const int T = P.T;
+
+  float2 h[NE][NA][ND];
+  float2* s_cm = s_dyn;
+  float2* s_ca = s_dyn + (size_t)P.nbt_max * AD * 8;
+
+  if (NE == 2) {
+    // ---- stage rotated coefficients: c'_l = c_l e^{-2 pi i l (k0 - origin)/N}
+    const float2* cm = args.coef + (size_t)u * coef_floats2(P);
+    const float2* ca = cm + (size_t)AD * P.n_blocks * 8;
+    const int b_first = k0 / P.block;
+    const int b_last = min(P.n_blocks - 1, (min(k0 + ARCHES_TILE, P.N) - 1) / P.block);
+    const int nbt = b_last - b_first + 1;  // MMSE blocks overlapping this tile (<= TILE/12)
+    for (int i = j; i < nbt * AD * 8; i += blockDim.x) {
+      const int bt = i / (AD * 8), r = i - bt * AD * 8, ad = r >> 3, l = r & 7;
+      const int b = b_first + bt;
+      const int off = k0 - b * P.block;  // may be negative
+      const int idx = (int)((((long long)l * off) % P.N + P.N) % P.N);
+      const float2 w = __ldg(&P.wN[idx]);  // e^{+2 pi i l off/N}; conj for synthesis
+      s_cm[bt * AD * 8 + r] = cmul(__ldg(&cm[((size_t)ad * P.n_blocks + b) * 8 + l]), make_float2(w.x, -w.y));
+    }
+    for (int i = j; i < AD * P.trunc; i += blockDim.x) {
+      const int l = i % P.trunc;
+      const int idx = (int)(((long long)l * k0) % P.N);
+      const float2 w = __ldg(&P.wN[idx]);
+      s_ca[i] = cmul(__ldg(&ca[i]), make_float2(w.x, -w.y));
+    }
+    __syncthreads();
+    const int bt = valid ? (k / P.block - b_first) : 0;
+    // ---- synthesis (twiddles e^{-2 pi i l j / N} from the plan table)
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int d = 0; d < ND; ++d) h[0][a][d] = h[1][a][d] = make_float2(0.f, 0.f);
+    for (int l = 0; l < P.trunc; ++l) {
+      const float2 w = __ldg(&P.syn[l * ARCHES_TILE + j]);
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        if (a < P.A)
+#pragma unroll
+          for (int d = 0; d < ND; ++d) cfma(h[0][a][d], s_ca[(a * ND + d) * P.trunc + l], w);
+      if (l < 8) {
+#pragma unroll
+        for (int a = 0; a < NA; ++a)
+          if (a < P.A)
+#pragma unroll
+            for (int d = 0; d < ND; ++d) cfma(h[1][a][d], s_cm[bt * AD * 8 + (a * ND + d) * 8 + l], w);
+      }
+    }
+    if (valid) {
+      const size_t ob = (size_t)u * AD * P.N + k;
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        if (a < P.A)
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          if (args.h_ai) args.h_ai[ob + (size_t)(a * ND + d) * P.N] = h[0][a][d];
+          if (args.h_mmse) args.h_mmse[ob + (size_t)(a * ND + d) * P.N] = h[1][a][d];
+        }
+    }
+  } else {
+    const size_t ob = (size_t)u * AD * P.N + (valid ? k : 0);
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int d = 0; d < ND; ++d)
+        h[0][a][d] = (valid && a < P.A) ? __ldg(&args.est[ob + (size_t)(a * ND + d) * P.N])
+                                        : make_float2(0.f, 0.f);
+  }
+
+  // ---- telemetry partials: sum |H|, sum |H|^2 per expert (expert index 0 = AI)
+  double v[11];
+#pragma unroll
+  for (int i = 0; i < 11; ++i) v[i] = 0.0;
+  if (valid) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      float sa = 0.f, sp = 0.f;
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          const float p2 = fmaf(h[e][a][d].x, h[e][a][d].x, h[e][a][d].y * h[e][a][d].y);
+          sa += sqrtf(p2);
+          sp += p2;
+        }
+      v[0 + e] = sa;
+      v[2 + e] = sp;
+    }
+    // ---- equaliser: interpolate in time, MRC over antennas, SINR sums in fp64
+    const float nv = (float)args.nv[u];
+    const size_t yb = (size_t)u * P.A * T * P.N + k;
+    const size_t xb = (size_t)u * T * P.N + k;
+    const bool even = (k & 1) == 0;
+    for (int t = 0; t < T; ++t) {
+      float2 yv[NA];
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        yv[a] = (a < P.A) ? __ldg(&args.y[yb + ((size_t)a * T + t) * P.N]) : make_float2(0.f, 0.f);
+      const float2 x = __ldg(&args.tx[xb + (size_t)t * P.N]);
+      const bool data = !(even && P.is_dmrs[t] >= 0);
+      float wt[ND];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) wt[d] = (d == P.tw_d0[t]) ? P.tw_w0[t] : ((d == P.tw_d1[t]) ? P.tw_w1[t] : 0.f);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        float2 num = make_float2(0.f, 0.f);
+        float den = 0.f;
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+          float2 hn = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int d = 0; d < ND; ++d) {
+            hn.x = fmaf(wt[d], h[e][a][d].x, hn.x);
+            hn.y = fmaf(wt[d], h[e][a][d].y, hn.y);
+          }
+          num.x = fmaf(hn.x, yv[a].x, fmaf(hn.y, yv[a].y, num.x));
+          num.y = fmaf(hn.x, yv[a].y, fmaf(-hn.y, yv[a].x, num.y));
+          den = fmaf(hn.x, hn.x, fmaf(hn.y, hn.y, den));
+        }
+        const float inv = 1.0f / (den + nv);
+        const float2 xh = make_float2(num.x * inv, num.y * inv);
+        if (args.x_hat) args.x_hat[xb + (size_t)t * P.N] = xh;
+        if (data) {
+          const double xr = x.x, xi = x.y, hr = xh.x, hi = xh.y;
+          v[5 + e] += xr * hr + xi * hi;   // Re conj(x) xh
+          v[7 + e] += xr * hi - xi * hr;   // Im conj(x) xh
+          v[9 + e] += hr * hr + hi * hi;
+        }
+      }
+      if (data) v[4] += (double)x.x * x.x + (double)x.y * x.y;
+    }
+  }
+  TilePartial* mine = args.parts + (size_t)u * gridDim.x + tile;
+  reduce_tile(v, s_scr, mine);
+  if (last_block_arrive(args.counters + u, gridDim.x, &s_flag) && threadIdx.x == 0) {
+    const int stream = u / args.n_slots;
+    const long long slot = args.first_slot + (u - stream * args.n_slots);
+    arches_telemetry tel;
+    finalize_unit(P, args.parts + (size_t)u * gridDim.x, gridDim.x,
+                  args.sigma2 ? args.sigma2 + u : nullptr, args.seeds ? args.seeds[stream] : 0ull,
+                  slot, NE, &tel);
+    if (args.tel) args.tel[u] = tel;
+    if (args.sinr_out) args.sinr_out[u] = tel.sinr_db[0];
+    if (args.abs_out) args.abs_out[u] = tel.abs_mean[0];
+    if (args.rsrp_out) args.rsrp_out[u] = tel.rsrp[0];
+  }
+}
+
+// compat synthesis of ONE expert from K1 coefficients: out[u][A][D][N]
+__global__ void k_synth_one(const PlanDev P, const float2* coef, int which /*1 mmse, 2 ai*/,
+                            float2* out) {
+  const int u = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P.N) return;
+  const int AD = P.A * P.D;
+  const float2* cm = coef + (size_t)u * coef_floats2(P);
+  const float2* ca = cm + (size_t)AD * P.n_blocks * 8;
+  const int b = min(k / P.block, P.n_blocks - 1);
+  const int kl = (which == 1) ? k - b * P.block : k;
+  const int nt = (which == 1) ? 8 : P.trunc;
+  for (int ad = 0; ad < AD; ++ad) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int l = 0; l < nt; ++l) {
+      const float2 c = (which == 1) ? cm[((size_t)ad * P.n_blocks + b) * 8 + l] : ca[ad * P.trunc + l];
+      const float2 w = __ldg(&P.wN[(int)(((long long)l * kl) % P.N)]);
+      cfma(acc, c, make_float2(w.x, -w.y));
+    }
+    out[((size_t)u * AD + ad) * P.N + k] = acc;
+  }
+}
