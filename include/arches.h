@@ -183,11 +183,13 @@ int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int32_t n_slot
  * |H|^2 reductions of run_slot (:453-455) and equalize (:253-279) for BOTH
  * experts in one pass over y/tx, then (last CTA per unit) link adaptation,
  * transport block, Philox CRC and LCID4 split for both candidates
- * (phy_pipeline.py:192-222,462-470).  Writes h_mmse, h_ai, tel. */
+ * (phy_pipeline.py:192-222,462-470).  Writes h_mmse, h_ai, tel.  Slot index of
+ * unit (stream, s) = first_slot + s, or, when first_slot < 0, the stream's
+ * device-resident next_slot (from `state`) + s -- graph-replayable. */
 int arches_experts_equalize(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                             const void* y, const void* tx, const double* noise_var,
-                            const uint64_t* seeds, int64_t first_slot, void* h_mmse,
-                            void* h_ai, arches_telemetry* tel, void* ws,
+                            const uint64_t* seeds, int64_t first_slot, const void* state,
+                            void* h_mmse, void* h_ai, arches_telemetry* tel, void* ws,
                             arches_stream_t stream);
 
 /* ---- K4: per-stream sequential KPM windows + control plane ----------
@@ -204,7 +206,8 @@ int arches_kpm_scan(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                     void* state, arches_kpm* kpm, arches_message* msg_log,
                     int32_t* msg_count, int32_t msg_cap, arches_stream_t stream);
 
-/* K1 + K2 + K4 for one batch (the per-step hot path). */
+/* K1 + K2 + K4 for one batch (the per-step hot path); first_slot < 0 takes the
+ * slot numbering from the device state (CUDA-graph friendly). */
 int arches_run_batch(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                      int64_t first_slot, const void* y, const void* tx, const void* pilots,
                      const double* noise_var, const uint64_t* seeds, const int8_t* regime,

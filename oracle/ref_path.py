@@ -40,7 +40,7 @@ def ls_estimate(y: np.ndarray, pil: np.ndarray, geo) -> np.ndarray:
         raise ConfigurationError("estimators support a single layer")
     if np.any(np.abs(pil) == 0):
         raise ContractViolation("pilot magnitude 0")
-    rows = y[:, 0::2, :][:, :, list(geo.dmrs_symbols)]          # (A, M, D)
+    rows = y[:, np.arange(0, geo.n_sc, 2), :][:, :, list(geo.dmrs_symbols)]   # (A, M, D)
     ratio = rows / pil[None, :, :]
     out = np.empty((geo.n_ant, 1, geo.n_sc, geo.n_dmrs), dtype=complex)
     out[:, 0, :, :] = ratio[:, np.arange(geo.n_sc) // 2, :]
@@ -49,7 +49,7 @@ def ls_estimate(y: np.ndarray, pil: np.ndarray, geo) -> np.ndarray:
 
 def estimate_noise_var(ls: np.ndarray, guard: int = 16) -> float:
     """expert_bank.py:199-214 -- mean tail power of the comb IFFT, times n_comb."""
-    comb = ls[:, :, 0::2, :]
+    comb = ls[:, :, np.arange(0, ls.shape[2], 2), :]   # fancy index: same layout as the reference
     m = comb.shape[2]
     if not 1 <= guard < m:
         raise ConfigurationError(f"guard {guard} outside 1..{m - 1}")
@@ -101,7 +101,9 @@ def mmse_estimate(ls: np.ndarray, noise_var: float, assumed_ds: float,
     n_sc = ls.shape[2]
     block = mmse_block(n_sc, block_prbs)
     w = wiener_matrix(n_sc, block, float(noise_var), float(assumed_ds))
-    comb = ls[:, :, 0::2, :]
+    mask = np.zeros(n_sc, dtype=bool)
+    mask[0::2] = True
+    comb = ls[:, :, mask, :]
     out = np.empty_like(ls)
     half = block // 2
     for b in range(n_sc // block):

@@ -386,12 +386,13 @@ static int launch_k2(const arches_plan* P, int n_units, const K2Args& a, cudaStr
 
 extern "C" int arches_experts_equalize(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                                        const void* y, const void* tx, const double* noise_var,
-                                       const uint64_t* seeds, int64_t first_slot, void* h_mmse,
-                                       void* h_ai, arches_telemetry* tel, void* ws,
-                                       arches_stream_t stream) {
+                                       const uint64_t* seeds, int64_t first_slot,
+                                       const void* state, void* h_mmse, void* h_ai,
+                                       arches_telemetry* tel, void* ws, arches_stream_t stream) {
   if (!plan || !y || !tx || !noise_var || !seeds || !ws || !tel || n_streams < 1 || n_slots < 1)
     return set_err(ARCHES_E_CONTRACT, "bad experts_equalize args");
-  if (first_slot < 0) return set_err(ARCHES_E_CONTRACT, "slot_index must be >= 0");
+  if (first_slot < 0 && !state)
+    return set_err(ARCHES_E_CONTRACT, "first_slot < 0 needs the stream state (slot source)");
   const int n_units = n_streams * n_slots;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const WsLayout w = ws_layout(plan, n_units);
@@ -409,6 +410,8 @@ extern "C" int arches_experts_equalize(const arches_plan* plan, int32_t n_stream
   a.parts = ws_at<TilePartial>(ws, w.parts);
   a.counters = ws_at<unsigned int>(ws, w.counters);
   a.tel = tel;
+  a.state = reinterpret_cast<const unsigned char*>(state);
+  a.state_stride = state_stride_bytes(plan->dev.window_length, plan->dev.dapp_window);
   a.first_slot = first_slot;
   a.n_slots = n_slots;
   return launch_k2<2>(plan, n_units, a, s);
@@ -443,7 +446,7 @@ extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int3
   int rc = arches_ls_analyze(plan, n_streams, n_slots, y, pilots, nullptr, ws, stream);
   if (rc) return rc;
   rc = arches_experts_equalize(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
-                               h_mmse, h_ai, tel, ws, stream);
+                               state, h_mmse, h_ai, tel, ws, stream);
   if (rc) return rc;
   return arches_kpm_scan(plan, n_streams, n_slots, tel, regime, tree, state, kpm, msg_log,
                          msg_count, msg_cap, stream);

@@ -131,7 +131,9 @@ struct K2Args {
   double* sinr_out;       // compat: [u] sinr / abs_mean / rsrp of expert 0
   double* abs_out;
   double* rsrp_out;
-  long long first_slot;
+  const unsigned char* state;  // per-stream control state (next_slot at offset 0)
+  size_t state_stride;
+  long long first_slot;         // < 0: take each stream's next_slot from `state`
   int n_slots;
 };
 
@@ -185,13 +187,16 @@ __global__ void __launch_bounds__(ARCHES_TILE)
     for (int a = 0; a < NA; ++a)
 #pragma unroll
       for (int d = 0; d < ND; ++d) h[0][a][d] = h[1][a][d] = make_float2(0.f, 0.f);
-    for (int l = 0; l < P.trunc; ++l) {
+    const int n_syn = max(P.trunc, 8);
+    for (int l = 0; l < n_syn; ++l) {
       const float2 w = __ldg(&P.syn[l * ARCHES_TILE + j]);
+      if (l < P.trunc) {
 #pragma unroll
-      for (int a = 0; a < NA; ++a)
-        if (a < P.A)
+        for (int a = 0; a < NA; ++a)
+          if (a < P.A)
 #pragma unroll
-          for (int d = 0; d < ND; ++d) cfma(h[0][a][d], s_ca[(a * ND + d) * P.trunc + l], w);
+            for (int d = 0; d < ND; ++d) cfma(h[0][a][d], s_ca[(a * ND + d) * P.trunc + l], w);
+      }
       if (l < 8) {
 #pragma unroll
         for (int a = 0; a < NA; ++a)
@@ -288,7 +293,10 @@ __global__ void __launch_bounds__(ARCHES_TILE)
   reduce_tile(v, s_scr, mine);
   if (last_block_arrive(args.counters + u, gridDim.x, &s_flag) && threadIdx.x == 0) {
     const int stream = u / args.n_slots;
-    const long long slot = args.first_slot + (u - stream * args.n_slots);
+    const long long base = args.first_slot >= 0
+        ? args.first_slot
+        : (long long)*reinterpret_cast<const int64_t*>(args.state + (size_t)stream * args.state_stride);
+    const long long slot = base + (u - stream * args.n_slots);
     arches_telemetry tel;
     finalize_unit(P, args.parts + (size_t)u * gridDim.x, gridDim.x,
                   args.sigma2 ? args.sigma2 + u : nullptr, args.seeds ? args.seeds[stream] : 0ull,

@@ -1,0 +1,269 @@
+"""Batched device engine: the performance path of the hot path.
+
+`ArchesPlan` wraps `arches_plan` (geometry + PipelineConfig + MMSE prior +
+control-plane configuration).  `SlotEngine` owns every device buffer for a
+batch of `n_streams` single-layer streams x `n_slots` consecutive slots and
+runs K1 -> K2 -> K4 (`arches_run_batch`) on the current torch CUDA stream,
+optionally through a captured CUDA graph.  Control state (mode, windows,
+pending messages, dApp window, fail-safe) stays device-resident across
+batches, so consecutive `run()` calls continue each stream's slot sequence
+exactly like repeated `Pipeline.run_slot` calls (phy_pipeline.py:422-493)
+driven by `harness.execute_run` (harness.py:174-231).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .config import DappConfig, ExecutionMode, LatencyModel, PipelineConfig
+from .errors import ConfigurationError, ContractViolation
+from .policy import to_device_struct
+from .scene import purpose_key
+
+
+def _policy_code(policy: str):
+    if policy == "oracle":
+        return _lib.POLICY_ORACLE, 0
+    if policy.startswith("fixed:"):
+        m = policy.split(":", 1)[1]
+        if m not in ("0", "1"):
+            raise ConfigurationError(f"fixed policy mode must be 0 or 1, got {m!r}")
+        return _lib.POLICY_FIXED, int(m)
+    if policy == "tree" or policy.startswith("tree:"):
+        return _lib.POLICY_TREE, 0
+    raise ConfigurationError(f"unknown policy source: {policy!r}")
+
+
+class ArchesPlan:
+    """Immutable per-configuration plan (device twiddle tables, MMSE Gram)."""
+
+    def __init__(self, geometry, assumed_delay_spread: float, pcfg: PipelineConfig | None = None,
+                 exec_mode: ExecutionMode = ExecutionMode.CONCURRENT, policy: str = "oracle",
+                 dapp: DappConfig | None = None, latency: LatencyModel | None = None):
+        if getattr(geometry, "n_layers", 1) != 1:
+            raise ConfigurationError("estimators support a single layer (one plan per layer port)")
+        pcfg = pcfg or PipelineConfig()
+        dapp = dapp or DappConfig()
+        latency = latency or LatencyModel()
+        self.geometry, self.pcfg, self.dapp, self.latency = geometry, pcfg, dapp, latency
+        self.exec_mode = ExecutionMode(exec_mode)
+        self.policy = policy
+        g = _lib.Geom()
+        g.n_ant, g.n_prb, g.n_sym = geometry.n_ant, geometry.n_prb, geometry.n_sym
+        syms = tuple(geometry.dmrs_symbols)
+        if len(syms) > _lib.MAX_DMRS:
+            raise ConfigurationError(f"at most {_lib.MAX_DMRS} DMRS symbols")
+        g.n_dmrs = len(syms)
+        for i, s in enumerate(syms):
+            g.dmrs_symbols[i] = s
+        g.slot_duration_us = float(geometry.slot_duration_us)
+        p = _lib.Params()
+        p.noise_guard = pcfg.noise_guard
+        p.truncation = min(pcfg.truncation, 12 * geometry.n_prb)   # run_slot :448
+        p.mmse_block_prbs = pcfg.mmse_block_prbs
+        p.window_length = pcfg.window_length
+        p.assumed_delay_spread = float(assumed_delay_spread)
+        p.ridge = 1e-12
+        p.sinr_cap_db = pcfg.sinr_cap_db
+        p.lcid4_fraction = pcfg.lcid4_fraction
+        p.lcid4_jitter = pcfg.lcid4_jitter
+        p.crc_margin_db = pcfg.crc_margin_db
+        p.crc_scale_db = pcfg.crc_scale_db
+        p.mac_header_bytes = pcfg.mac_header_bytes
+        t = pcfg.mcs_table
+        if t.n_mcs > _lib.MAX_MCS:
+            raise ConfigurationError(f"at most {_lib.MAX_MCS} MCS rows")
+        p.n_mcs = t.n_mcs
+        for i in range(t.n_mcs):
+            p.mcs_threshold_db[i] = t.thresholds_db[i]
+            p.mcs_qam[i] = t.qam_order[i]
+            p.mcs_rate[i] = t.code_rate[i]
+        p.exec_mode = (_lib.EXEC_SELECTED_ONLY if self.exec_mode is ExecutionMode.SELECTED_ONLY
+                       else _lib.EXEC_CONCURRENT)
+        p.policy, p.fixed_mode = _policy_code(policy)
+        p.decision_period_slots = dapp.decision_period_slots
+        p.dapp_window_slots = dapp.window_length_slots
+        p.decision_delay_ns = latency.decision_delay_ns()
+        p.failsafe_timeout_ns = dapp.timeout_ns(geometry.slot_duration_ns)
+        p.crc_purpose_key = purpose_key("crc")
+        self._geom, self._params = g, p
+        h = C.c_void_p()
+        _lib.check(_lib.lib().arches_plan_create(C.byref(g), C.byref(p), C.byref(h)))
+        self.handle = h
+
+    @property
+    def n_sc(self):
+        return 12 * self.geometry.n_prb
+
+    def state_bytes(self, n_streams: int) -> int:
+        return _lib.lib().arches_state_bytes(self.handle, n_streams)
+
+    def workspace_bytes(self, n_units: int) -> int:
+        return _lib.lib().arches_workspace_bytes(self.handle, n_units)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.lib().arches_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _stream_handle():
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+class SlotEngine:
+    """Device buffers + launches for one batch shape (n_streams x n_slots)."""
+
+    def __init__(self, plan: ArchesPlan, n_streams: int, n_slots: int, tree=None,
+                 msg_cap: int = 4096, device: str = "cuda"):
+        import torch
+        if n_streams < 1 or n_slots < 1:
+            raise ConfigurationError("n_streams and n_slots must be >= 1")
+        self.plan, self.S, self.C = plan, n_slots, n_streams
+        self.U = n_streams * n_slots
+        geo = plan.geometry
+        A, T, N, D = geo.n_ant, geo.n_sym, 12 * geo.n_prb, len(geo.dmrs_symbols)
+        self.A, self.T, self.N, self.D, self.M = A, T, N, D, N // 2
+        dev = torch.device(device)
+        self.device = dev
+        U = self.U
+        self.y = torch.zeros((U, A, T, N), dtype=torch.complex64, device=dev)
+        self.tx = torch.zeros((U, T, N), dtype=torch.complex64, device=dev)
+        self.pilots = torch.zeros((n_streams, self.M, D), dtype=torch.complex64, device=dev)
+        self.noise_var = torch.zeros(U, dtype=torch.float64, device=dev)
+        self.regime = torch.ones(U, dtype=torch.int8, device=dev)
+        self.seeds = torch.zeros(n_streams, dtype=torch.int64, device=dev)
+        self.h_mmse = torch.zeros((U, A, D, N), dtype=torch.complex64, device=dev)
+        self.h_ai = torch.zeros((U, A, D, N), dtype=torch.complex64, device=dev)
+        self.tel = torch.zeros(U * _lib.TELEMETRY_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        self.kpm = torch.zeros(U * _lib.KPM_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        self.msg_cap = msg_cap
+        self.msg_log = torch.zeros(n_streams * msg_cap * _lib.MESSAGE_DTYPE.itemsize,
+                                   dtype=torch.uint8, device=dev)
+        self.msg_count = torch.zeros(n_streams, dtype=torch.int32, device=dev)
+        self.state = torch.zeros(plan.state_bytes(n_streams), dtype=torch.uint8, device=dev)
+        self.ws = torch.zeros(plan.workspace_bytes(U), dtype=torch.uint8, device=dev)
+        self.tree = None
+        if tree is not None:
+            raw = bytes(to_device_struct(tree))
+            self.tree = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
+        elif plan.policy.startswith("tree"):
+            raise ConfigurationError("tree policy needs a tree")
+        self.next_slot = 0
+        self.graph = None
+        self.reset()
+
+    # ------------------------------------------------------------ state
+    def reset(self):
+        _lib.check(_lib.lib().arches_state_init(self.plan.handle, _lib.ptr(self.state), self.C,
+                                                _stream_handle()))
+        self.msg_count.zero_()
+        self.next_slot = 0
+
+    def set_streams(self, pilots: np.ndarray, seeds):
+        """pilots (n_streams, M, D) complex; seeds (n_streams,) scenario seeds."""
+        import torch
+        p = np.asarray(pilots)
+        if p.shape != (self.C, self.M, self.D):
+            raise ContractViolation(f"pilots shape {p.shape}, expected {(self.C, self.M, self.D)}")
+        if np.any(np.abs(p) == 0):
+            raise ContractViolation("pilot magnitude 0")
+        self.pilots.copy_(torch.from_numpy(p.astype(np.complex64)))
+        s = np.asarray([int(v) & ((1 << 64) - 1) for v in seeds], dtype=np.uint64).view(np.int64)
+        self.seeds.copy_(torch.from_numpy(s))
+
+    def load(self, y=None, tx=None, noise_var=None, regime=None, non_blocking=False):
+        """Copy one batch of inputs (host or device tensors / numpy) into the engine.
+        y: (U, A, T, N) complex64 device layout; tx: (U, T, N); noise_var: (U,);
+        regime: (U,) 1 = good."""
+        import torch
+
+        def put(dst, src, dtype):
+            if src is None:
+                return
+            t = src if isinstance(src, torch.Tensor) else torch.from_numpy(np.asarray(src, dtype=dtype))
+            if tuple(t.shape) != tuple(dst.shape):
+                raise ContractViolation(f"shape {tuple(t.shape)}, expected {tuple(dst.shape)}")
+            dst.copy_(t, non_blocking=non_blocking)
+
+        put(self.y, y, np.complex64)
+        put(self.tx, tx, np.complex64)
+        put(self.noise_var, noise_var, np.float64)
+        put(self.regime, regime, np.int8)
+
+    # ------------------------------------------------------------ run
+    def _launch(self, first_slot: int):
+        L = _lib.lib()
+        _lib.check(L.arches_run_batch(
+            self.plan.handle, self.C, self.S, first_slot, _lib.ptr(self.y), _lib.ptr(self.tx),
+            _lib.ptr(self.pilots), _lib.ptr(self.noise_var), _lib.ptr(self.seeds),
+            _lib.ptr(self.regime), _lib.ptr(self.tree), _lib.ptr(self.state),
+            _lib.ptr(self.h_mmse), _lib.ptr(self.h_ai), _lib.ptr(self.tel), _lib.ptr(self.kpm),
+            _lib.ptr(self.msg_log), _lib.ptr(self.msg_count), self.msg_cap, _lib.ptr(self.ws),
+            _stream_handle()))
+
+    def run(self):
+        """Process the loaded batch (slots next_slot .. next_slot + n_slots - 1).
+        Slot numbering is read from the device-resident state, so the launch
+        sequence is identical every step and can be replayed as a CUDA graph."""
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch(-1)
+        self.next_slot += self.S
+
+    def capture_graph(self):
+        """Capture K1 -> K2 -> K4 once; later run() calls replay it."""
+        import torch
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self._launch(-1)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+
+    def launches_per_run(self) -> int:
+        return 3  # K1, K2, K4 (+ one memset node)
+
+    def switch_copy(self):
+        """K5: reference aliasing semantics -- copy MMSE into the AI buffer for mode-1 units."""
+        _lib.check(_lib.lib().arches_switch_copy(self.plan.handle, self.U, _lib.ptr(self.kpm),
+                                                 _lib.ptr(self.h_mmse), _lib.ptr(self.h_ai),
+                                                 _stream_handle()))
+
+    # ------------------------------------------------------------ results
+    def kpm_records(self) -> np.ndarray:
+        return self.kpm.cpu().numpy().view(_lib.KPM_DTYPE).reshape(self.C, self.S)
+
+    def telemetry(self) -> np.ndarray:
+        return self.tel.cpu().numpy().view(_lib.TELEMETRY_DTYPE).reshape(self.C, self.S)
+
+    def messages(self, stream: int = 0) -> np.ndarray:
+        """Control messages of one stream in emission order (ControlMessage log of
+        execute_run, harness.py:184-226).  The fixed policy's t=0 message is a
+        configuration event and is reported first."""
+        n = int(self.msg_count[stream].item())
+        raw = self.msg_log.view(self.C, -1)[stream].cpu().numpy().view(_lib.MESSAGE_DTYPE)
+        out = raw[:min(n, self.msg_cap)]
+        if self.plan.policy.startswith("fixed:"):
+            first = np.zeros(1, dtype=_lib.MESSAGE_DTYPE)
+            first["mode"] = int(self.plan.policy.split(":")[1])
+            first["trigger"] = 3
+            out = np.concatenate([first, out])
+        return out
+
+    def downstream(self, unit: int):
+        """Switch predicate applied: the estimate consumers read for `unit` (A, D, N)."""
+        mode = int(self.kpm_records().reshape(-1)[unit]["mode"])
+        return self.h_mmse[unit] if mode == 1 else self.h_ai[unit]
