@@ -206,6 +206,15 @@ int arches_kpm_scan(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                     void* state, arches_kpm* kpm, arches_message* msg_log,
                     int32_t* msg_count, int32_t msg_cap, arches_stream_t stream);
 
+/* Same contract and results as arches_kpm_scan, one thread walking every slot
+ * of a stream (the literal restatement; the default scan is warp-parallel).
+ * Kept exported so parity tests can cross-check the two forms. */
+int arches_kpm_scan_sequential(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                               const arches_telemetry* tel, const int8_t* regime,
+                               const arches_tree* tree, void* state, arches_kpm* kpm,
+                               arches_message* msg_log, int32_t* msg_count, int32_t msg_cap,
+                               arches_stream_t stream);
+
 /* K1 + K2 + K4 for one batch (the per-step hot path); first_slot < 0 takes the
  * slot numbering from the device state (CUDA-graph friendly). */
 int arches_run_batch(const arches_plan* plan, int32_t n_streams, int32_t n_slots,

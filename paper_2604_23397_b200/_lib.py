@@ -77,6 +77,8 @@ _SIGS = {
     "arches_experts_equalize": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, P, C.c_int64, P, P,
                                           P, P, P, P]),
     "arches_kpm_scan": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, P, P, P, P, C.c_int32, P]),
+    "arches_kpm_scan_sequential": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, P, P, P, P,
+                                             C.c_int32, P]),
     "arches_run_batch": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P, P,
                                    P, P, P, P, P, P, C.c_int32, P, P]),
     "arches_switch_copy": (C.c_int, [P, C.c_int32, P, P, P, P]),

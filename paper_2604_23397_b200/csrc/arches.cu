@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "k_analyze.cuh"
 #include "k_control.cuh"
+#include "k_control_warp.cuh"
 #include "k_synth_eq.cuh"
 #include "rng.cuh"
 
@@ -423,6 +424,25 @@ extern "C" int arches_kpm_scan(const arches_plan* plan, int32_t n_streams, int32
                                const arches_tree* tree, void* state, arches_kpm* kpm,
                                arches_message* msg_log, int32_t* msg_count, int32_t msg_cap,
                                arches_stream_t stream) {
+  if (!plan || !tel || !state || !kpm || n_streams < 1 || n_slots < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad kpm_scan args");
+  if (plan->dev.policy == ARCHES_POLICY_TREE && !tree)
+    return set_err(ARCHES_E_CONTRACT, "tree policy needs a tree");
+  if (plan->dev.policy == ARCHES_POLICY_ORACLE && !regime)
+    return set_err(ARCHES_E_CONTRACT, "oracle policy needs the regime timeline");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  K4Args a{tel, regime, tree, state, kpm, msg_log, msg_count, msg_cap, n_streams, n_slots};
+  k4_kpm_scan_warp<<<n_streams, 32, 0, s>>>(plan->dev, a);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_kpm_scan_sequential(const arches_plan* plan, int32_t n_streams,
+                                          int32_t n_slots, const arches_telemetry* tel,
+                                          const int8_t* regime, const arches_tree* tree,
+                                          void* state, arches_kpm* kpm, arches_message* msg_log,
+                                          int32_t* msg_count, int32_t msg_cap,
+                                          arches_stream_t stream) {
   if (!plan || !tel || !state || !kpm || n_streams < 1 || n_slots < 1)
     return set_err(ARCHES_E_CONTRACT, "bad kpm_scan args");
   if (plan->dev.policy == ARCHES_POLICY_TREE && !tree)

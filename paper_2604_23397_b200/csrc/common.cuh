@@ -76,9 +76,9 @@ struct StreamState {
   int64_t mac_total, l4_total;
   int64_t last_delivery_ns;
   int32_t mode, ndi;
-  int32_t win_fill, win_head;
+  int32_t reserved1, reserved2;
   int32_t n_pending, n_forced;
-  int32_t since_decision, feat_fill, feat_head, tripped;
+  int32_t since_decision, reserved3, reserved4, tripped;
   int32_t last_msg_mode, pad;
   PendingMsg pending[ARCHES_MAX_PENDING];
   PendingMsg forced[ARCHES_MAX_PENDING];

@@ -50,11 +50,14 @@ __device__ inline void queue_pop_front(PendingMsg* q, int32_t& n) {
   --n;
 }
 
-__device__ inline double window_push(int32_t* ring, int64_t& total, int fill_before, int head,
-                                     int window, int32_t nbytes, double slot_s) {
+// ThroughputWindow.push (phy_pipeline.py:334-340) with the ring indexed by push
+// count n (ring[n % W] holds the value pushed W slots ago until overwritten)
+__device__ inline double window_push(int32_t* ring, int64_t& total, int64_t n, int window,
+                                     int32_t nbytes, double slot_s) {
   total += nbytes;
-  if (fill_before == window) total -= ring[head];
-  const int filled = min(fill_before + 1, window);
+  if (n >= window) total -= ring[n % window];
+  ring[n % window] = nbytes;
+  const int filled = (int)min((int64_t)window, n + 1);
   return xdiv(xdiv(xmul((double)total, 8.0), 1e6), xmul((double)filled, slot_s));
 }
 
@@ -123,17 +126,8 @@ __global__ void k4_kpm_scan(const PlanDev P, const K4Args a) {
     const int pdu = max(tb - P.mac_header_bytes, 0);
     const int mac_rx = tl.mac_rx[e], l4_rx = tl.lcid4_rx[e];
     if (crc) st.cum_phy_bytes += tb;
-    const double mac_t = window_push(sv.mac_ring, st.mac_total, st.win_fill, st.win_head, W, mac_rx, P.slot_s);
-    const double l4_t = window_push(sv.l4_ring, st.l4_total, st.win_fill, st.win_head, W, l4_rx, P.slot_s);
-    if (st.win_fill == W) {
-      sv.mac_ring[st.win_head] = mac_rx;
-      sv.l4_ring[st.win_head] = l4_rx;
-      st.win_head = (st.win_head + 1 == W) ? 0 : st.win_head + 1;
-    } else {
-      sv.mac_ring[st.win_fill] = mac_rx;
-      sv.l4_ring[st.win_fill] = l4_rx;
-      ++st.win_fill;
-    }
+    const double mac_t = window_push(sv.mac_ring, st.mac_total, n, W, mac_rx, P.slot_s);
+    const double l4_t = window_push(sv.l4_ring, st.l4_total, n, W, l4_rx, P.slot_s);
     const double elapsed = xmul(xmul((double)(n + 1), P.slot_us), 1e-6);
     const double phy_t = xdiv(xdiv(xmul((double)st.cum_phy_bytes, 8.0), 1e6), elapsed);
     const int ndi = st.ndi;
@@ -170,14 +164,7 @@ __global__ void k4_kpm_scan(const PlanDev P, const K4Args a) {
       }
     } else if (P.policy == ARCHES_POLICY_TREE) {
       // Dapp.on_indication: append the record's features to the window
-      double* row;
-      if (st.feat_fill == WD) {
-        row = sv.feat + (size_t)st.feat_head * ARCHES_FEATURES;
-        st.feat_head = (st.feat_head + 1 == WD) ? 0 : st.feat_head + 1;
-      } else {
-        row = sv.feat + (size_t)st.feat_fill * ARCHES_FEATURES;
-        ++st.feat_fill;
-      }
+      double* row = sv.feat + (size_t)(n % WD) * ARCHES_FEATURES;
       row[0] = phy_t;
       row[1] = (double)mcs;
       row[2] = (double)pdu;
@@ -191,15 +178,13 @@ __global__ void k4_kpm_scan(const PlanDev P, const K4Args a) {
       if (++st.since_decision >= P.decision_period) {
         st.since_decision = 0;
         double feat[ARCHES_FEATURES];
-        const int first = (st.feat_fill == WD) ? st.feat_head : 0;
+        const int rows = (int)min((int64_t)WD, n + 1);
         for (int f = 0; f < ARCHES_FEATURES; ++f) feat[f] = 0.0;
-        for (int i = 0; i < st.feat_fill; ++i) {
-          int idx = first + i;
-          if (idx >= WD) idx -= WD;
-          const double* rw = sv.feat + (size_t)idx * ARCHES_FEATURES;
+        for (int i = 0; i < rows; ++i) {
+          const double* rw = sv.feat + (size_t)((n - rows + 1 + i) % WD) * ARCHES_FEATURES;
           for (int f = 0; f < ARCHES_FEATURES; ++f) feat[f] = xadd(feat[f], rw[f]);
         }
-        for (int f = 0; f < ARCHES_FEATURES; ++f) feat[f] = xdiv(feat[f], (double)st.feat_fill);
+        for (int f = 0; f < ARCHES_FEATURES; ++f) feat[f] = xdiv(feat[f], (double)rows);
         const int mode = tree_descend(a.tree, feat);
         const int64_t decided = end_ns + P.decision_delay_ns;
         PendingMsg m = {decided, mode, ARCHES_TRIGGER_POLICY};

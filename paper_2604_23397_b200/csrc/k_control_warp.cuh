@@ -1,0 +1,240 @@
+// K4 (warp form) -- one warp per stream; slot-parallel KPM derivation.
+//
+// Same semantics as k4_kpm_scan (k_control.cuh), restructured so only the
+// control plane stays sequential:
+//   1. lane 0 walks up to 32 slots applying SwitchController.begin_slot, the
+//      oracle message source and the fail-safe (integer ns, cheap) and stops
+//      early at a dApp decision slot -- the only event that needs KPMs;
+//   2. all lanes derive their slot's KPM record in parallel: cumulative PHY
+//      bytes / NDI parity / MAC + LCID4 window totals are warp prefix scans,
+//      the throughput divisions are per-lane fp64 with CPython rounding;
+//   3. at a decision slot lanes 0..9 form the window-mean features (sequential
+//      fp64 column sums in slot order, as numpy's axis-0 mean), lane 0 runs the
+//      tree and queues the ControlMessage.
+// Rings are indexed by push count: mac/l4 values at [n % W], features at
+// [n % WD] (n = slot index since stream start == pushes so far).
+#pragma once
+#include "k_control.cuh"
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(32) k4_kpm_scan_warp(const PlanDev P, const K4Args a) {
+  const int stream = blockIdx.x;
+  const int lane = threadIdx.x;
+  if (stream >= a.n_streams) return;
+  __shared__ int s_mode[32];
+  __shared__ int s_len, s_decide;
+  __shared__ StreamState s_st;
+  StateView sv = state_view(a.state, stream, P.window_length, P.dapp_window);
+  if (lane == 0) s_st = *sv.h;
+  __syncwarp();
+  const int W = P.window_length, WD = P.dapp_window;
+  const int64_t slot_ns = P.slot_ns;
+  int s0 = 0;
+  while (s0 < a.n_slots) {
+    // ---------------- 1. sequential control walk (lane 0)
+    if (lane == 0) {
+      StreamState& st = s_st;
+      int j = 0, decide = 0;
+      for (; j < 32 && s0 + j < a.n_slots; ++j) {
+        const int64_t n = st.next_slot + j;
+        const int64_t t0 = n * slot_ns;
+        const int64_t cut = (P.exec_mode == ARCHES_EXEC_SELECTED_ONLY) ? t0 - slot_ns : t0;
+        while (st.n_pending > 0 && st.pending[0].at_ns <= cut) {
+          st.mode = st.pending[0].mode;
+          queue_pop_front(st.pending, st.n_pending);
+        }
+        while (st.n_forced > 0 && st.forced[0].at_ns <= t0) {
+          st.mode = st.forced[0].mode;
+          queue_pop_front(st.forced, st.n_forced);
+        }
+        s_mode[j] = st.mode;
+        const int64_t end_ns = (n + 1) * slot_ns;
+        if (P.policy == ARCHES_POLICY_ORACLE) {
+          const int u = stream * a.n_slots + s0 + j;
+          const int want = (a.regime && a.regime[u]) ? 1 : 0;
+          if (want != st.last_msg_mode) {
+            PendingMsg m = {end_ns, want, ARCHES_TRIGGER_ORACLE};
+            queue_insert(st.pending, st.n_pending, m);
+            st.last_msg_mode = want;
+            log_message(a.msg_log, a.msg_count, a.msg_cap, stream, want, end_ns, end_ns,
+                        ARCHES_TRIGGER_ORACLE);
+          }
+        } else if (P.policy == ARCHES_POLICY_TREE) {
+          if (++st.since_decision >= P.decision_period) {
+            decide = 1;  // features of slots <= n needed: stop the walk here
+            ++j;
+            break;
+          }
+          if (!st.tripped && end_ns - st.last_delivery_ns > P.failsafe_timeout_ns && st.mode != 1) {
+            st.tripped = 1;
+            PendingMsg f = {end_ns, 1, ARCHES_TRIGGER_FAILSAFE};
+            queue_insert(st.forced, st.n_forced, f);
+            log_message(a.msg_log, a.msg_count, a.msg_cap, stream, 1, end_ns, end_ns,
+                        ARCHES_TRIGGER_FAILSAFE);
+          }
+        }
+      }
+      s_len = j;
+      s_decide = decide;
+    }
+    __syncwarp();
+    const int len = s_len;
+    const int decide = s_decide;
+    const int64_t n0 = s_st.next_slot;
+    // ---------------- 2. slot-parallel KPM derivation
+    const bool act = lane < len;
+    const int64_t n = n0 + lane;
+    const int u = stream * a.n_slots + s0 + lane;
+    int e = 0, mcs = 0, tb = 0, crc = 0, mac_rx = 0, l4_rx = 0, ncb = 1;
+    double rsrp = 0.0, snr = 0.0, absm = 0.0;
+    if (act) {
+      e = s_mode[lane];
+      const arches_telemetry& tl = a.tel[u];
+      mcs = tl.mcs[e];
+      tb = tl.tb_bytes[e];
+      crc = tl.crc[e];
+      mac_rx = tl.mac_rx[e];
+      l4_rx = tl.lcid4_rx[e];
+      ncb = tl.num_cb[e];
+      rsrp = tl.rsrp[e];
+      snr = tl.sinr_db[e];
+      absm = tl.abs_mean[e];
+    }
+    // evicted window values (pushed W slots earlier), ring indexed by n % W
+    int32_t sh_mac = 0, sh_l4 = 0;
+    if (W < 32) {  // warp-uniform: the evicted value may come from this chunk
+      sh_mac = __shfl_sync(0xffffffffu, mac_rx, (lane - W) & 31);
+      sh_l4 = __shfl_sync(0xffffffffu, l4_rx, (lane - W) & 31);
+    }
+    int32_t ev_mac = 0, ev_l4 = 0;
+    if (act && n >= W) {
+      if (lane >= W) {
+        ev_mac = sh_mac;
+        ev_l4 = sh_l4;
+      } else {
+        ev_mac = sv.mac_ring[n % W];
+        ev_l4 = sv.l4_ring[n % W];
+      }
+    }
+    const long long d_mac = act ? (long long)mac_rx - ev_mac : 0;
+    const long long d_l4 = act ? (long long)l4_rx - ev_l4 : 0;
+    const long long d_phy = (act && crc) ? (long long)tb : 0;
+    const int c_crc = (act && crc) ? 1 : 0;
+    const long long mac_tot = s_st.mac_total + warp_incl_scan(d_mac, lane);
+    const long long l4_tot = s_st.l4_total + warp_incl_scan(d_l4, lane);
+    const long long cum = s_st.cum_phy_bytes + warp_incl_scan(d_phy, lane);
+    const int crc_incl = warp_incl_scan(c_crc, lane);
+    const int ndi = s_st.ndi ^ ((crc_incl - c_crc) & 1);
+    __syncwarp();
+    if (act) {
+      const int filled = (int)min((long long)W, (long long)n + 1);
+      const double denom = xmul((double)filled, P.slot_s);
+      const double mac_t = xdiv(xdiv(xmul((double)mac_tot, 8.0), 1e6), denom);
+      const double l4_t = xdiv(xdiv(xmul((double)l4_tot, 8.0), 1e6), denom);
+      const double elapsed = xmul(xmul((double)(n + 1), P.slot_us), 1e-6);
+      const double phy_t = xdiv(xdiv(xmul((double)cum, 8.0), 1e6), elapsed);
+      const int pdu = max(tb - P.mac_header_bytes, 0);
+      arches_kpm r;
+      r.slot_index = n;
+      r.phy_throughput = phy_t;
+      r.rsrp = rsrp;
+      r.code_rate = P.mcs_rate[mcs];
+      r.snr_db = snr;
+      r.mac_throughput = mac_t;
+      r.lcid4_throughput = l4_t;
+      r.est_abs_mean = absm;
+      r.mcs_index = mcs;
+      r.pdu_length = pdu;
+      r.ndi = ndi;
+      r.qam_order = P.mcs_qam[mcs];
+      r.num_cb = ncb;
+      r.tb_size = tb;
+      r.mac_rx_bytes = mac_rx;
+      r.lcid4_rx_bytes = l4_rx;
+      r.mode = e;
+      r.crc_pass = crc;
+      a.kpm[u] = r;
+      // ring updates: the last lane mapping to a slot wins (only matters for W < 32)
+      if (lane + W >= len) {
+        sv.mac_ring[n % W] = mac_rx;
+        sv.l4_ring[n % W] = l4_rx;
+      }
+      if (P.policy == ARCHES_POLICY_TREE && lane + WD >= len) {
+        double* row = sv.feat + (size_t)(n % WD) * ARCHES_FEATURES;
+        row[0] = phy_t;
+        row[1] = (double)mcs;
+        row[2] = (double)pdu;
+        row[3] = (double)ndi;
+        row[4] = rsrp;
+        row[5] = snr;
+        row[6] = mac_t;
+        row[7] = l4_t;
+        row[8] = (double)mac_rx;
+        row[9] = (double)l4_rx;
+      }
+    }
+    // carry the chunk totals (last active lane)
+    const int last = len - 1;
+    const long long mac_c = __shfl_sync(0xffffffffu, mac_tot, last);
+    const long long l4_c = __shfl_sync(0xffffffffu, l4_tot, last);
+    const long long cum_c = __shfl_sync(0xffffffffu, cum, last);
+    const int ndi_next = __shfl_sync(0xffffffffu, ndi ^ c_crc, last);
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) {
+      s_st.mac_total = mac_c;
+      s_st.l4_total = l4_c;
+      s_st.cum_phy_bytes = cum_c;
+      s_st.ndi = ndi_next;
+      s_st.next_slot = n0 + len;
+    }
+    __syncwarp();
+    // ---------------- 3. dApp decision at the chunk's last slot
+    if (decide) {
+      __shared__ double s_feat[ARCHES_FEATURES];
+      const int64_t nd = n0 + len - 1;
+      const int rows = (int)min((long long)WD, (long long)nd + 1);
+      if (lane < ARCHES_FEATURES) {
+        double acc = 0.0;
+        for (int i = 0; i < rows; ++i) {
+          const int64_t p = nd - rows + 1 + i;  // oldest first
+          acc = xadd(acc, sv.feat[(size_t)(p % WD) * ARCHES_FEATURES + lane]);
+        }
+        s_feat[lane] = xdiv(acc, (double)rows);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        StreamState& st = s_st;
+        st.since_decision = 0;
+        const int64_t end_ns = (nd + 1) * slot_ns;
+        const int mode = tree_descend(a.tree, s_feat);
+        const int64_t decided = end_ns + P.decision_delay_ns;
+        PendingMsg m = {decided, mode, ARCHES_TRIGGER_POLICY};
+        queue_insert(st.pending, st.n_pending, m);
+        st.last_delivery_ns = max(st.last_delivery_ns, decided);
+        st.tripped = 0;
+        log_message(a.msg_log, a.msg_count, a.msg_cap, stream, mode, decided, decided,
+                    ARCHES_TRIGGER_POLICY);
+        if (!st.tripped && end_ns - st.last_delivery_ns > P.failsafe_timeout_ns && st.mode != 1) {
+          st.tripped = 1;
+          PendingMsg f = {end_ns, 1, ARCHES_TRIGGER_FAILSAFE};
+          queue_insert(st.forced, st.n_forced, f);
+          log_message(a.msg_log, a.msg_count, a.msg_cap, stream, 1, end_ns, end_ns,
+                      ARCHES_TRIGGER_FAILSAFE);
+        }
+      }
+      __syncwarp();
+    }
+    s0 += len;
+  }
+  if (lane == 0) *sv.h = s_st;
+}
