@@ -49,11 +49,12 @@ struct arches_plan {
   arches_geom g;
   arches_params p;
   PlanDev dev;
-  int k1_chunk;     // K1 points per chunk
-  int k1_per_chunk; // blocked MMSE: per-block bins
+  int k1_chunk;        // K1 points per CTA (comb analysis)
+  int k1_parts;        // K1 CTAs per unit (comb analysis)
   size_t k1_smem;
-  size_t k1_full_smem;  // N-point (denoiser compat) variant
-  int k1_full_chunk;
+  int k1_full_chunk;   // N-point (denoiser compat) variant
+  int k1_full_parts;
+  size_t k1_full_smem;
   size_t k2_smem;
   void* dev_tables;
 };
@@ -62,7 +63,7 @@ static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // ------------------------------------------------------------ workspace
 struct WsLayout {
-  size_t coef, parts, counters, block_bins, sigma2, total;
+  size_t coef, parts, counters, k1parts, k1counters, sigma2, total;
 };
 
 static WsLayout ws_layout(const arches_plan* P, int n_units) {
@@ -75,8 +76,13 @@ static WsLayout ws_layout(const arches_plan* P, int n_units) {
   off += align256((size_t)n_units * d.n_tiles * sizeof(TilePartial));
   w.counters = off;
   off += align256((size_t)n_units * sizeof(unsigned int));
-  w.block_bins = off;
-  if (P->k1_per_chunk) off += align256((size_t)n_units * d.n_blocks * d.A * d.D * 8 * sizeof(double2));
+  w.k1parts = off;
+  {
+    const int np = std::max(P->k1_parts, P->k1_full_parts);
+    off += align256((size_t)n_units * np * (2 * (size_t)d.A * d.D * d.L + 2) * sizeof(double));
+  }
+  w.k1counters = off;
+  off += align256((size_t)n_units * sizeof(unsigned int));
   w.sigma2 = off;
   off += align256((size_t)n_units * sizeof(double));
   w.total = off;
@@ -279,19 +285,25 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
 
   // ---- K1 launch geometry
   const int AD = d.A * d.D;
-  P->k1_per_chunk = (!d.diag && d.n_blocks > 1) ? 1 : 0;
   int chunk = std::max(32, std::min(256, (8192 / AD) / 32 * 32));
-  if (P->k1_per_chunk) chunk = pil_per_block;
+  if (d.n_blocks > 1) chunk = pil_per_block;  // one CTA per MMSE block
   P->k1_chunk = chunk;
+  P->k1_parts = (M + chunk - 1) / chunk;
   auto k1_smem = [&](int ch) {
     const size_t stage = std::max((size_t)AD * ch, (size_t)ARCHES_K1_THREADS * ARCHES_RA * ARCHES_RL);
-    return stage * sizeof(float2) + (size_t)AD * d.L * sizeof(double2) + 64 * sizeof(double) +
-           64 * sizeof(double2);
+    return stage * sizeof(float2) + (size_t)AD * d.L * sizeof(double2) + 64 * sizeof(double2);
   };
   P->k1_smem = k1_smem(chunk);
   P->k1_full_chunk = std::max(32, std::min(256, (8192 / AD) / 32 * 32));
+  P->k1_full_parts = (N + P->k1_full_chunk - 1) / P->k1_full_chunk;
   P->k1_full_smem = k1_smem(P->k1_full_chunk);
-  P->k2_smem = ((size_t)d.nbt_max * AD * 8 + (size_t)AD * d.trunc) * sizeof(float2);
+  P->k2_smem = ((size_t)(d.A + 1) * d.T * ARCHES_TILE + (size_t)d.nbt_max * AD * 8 +
+                (size_t)AD * d.trunc) * sizeof(float2);
+  if (P->k2_smem > 200 * 1024) {
+    cudaFree(buf);
+    delete P;
+    return set_err(ARCHES_E_CONFIG, "K2 tile does not fit shared memory (n_ant too large)");
+  }
   *out = P;
   return ARCHES_OK;
 }
@@ -326,16 +338,11 @@ extern "C" int arches_state_init(const arches_plan* plan, void* state, int32_t n
 // ------------------------------------------------------------ K1
 template <class Src>
 static int launch_k1(const arches_plan* P, int n_units, const Src& src, const K1Out& o, int npts,
-                     int chunk, size_t smem, bool per_chunk, cudaStream_t s) {
-  if (per_chunk) {
-    auto kern = k1_analyze<Src, true>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<n_units, ARCHES_K1_THREADS, smem, s>>>(P->dev, src, o, npts, chunk);
-  } else {
-    auto kern = k1_analyze<Src, false>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<n_units, ARCHES_K1_THREADS, smem, s>>>(P->dev, src, o, npts, chunk);
-  }
+                     int chunk, size_t smem, cudaStream_t s) {
+  auto kern = k1_analyze<Src>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((npts + chunk - 1) / chunk, n_units);
+  kern<<<grid, ARCHES_K1_THREADS, smem, s>>>(P->dev, src, o, npts, chunk);
   LAUNCH_CHECK();
   return ARCHES_OK;
 }
@@ -349,11 +356,11 @@ extern "C" int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const WsLayout w = ws_layout(plan, n_units);
   GridCombSrc src{reinterpret_cast<const float2*>(y), reinterpret_cast<const float2*>(pilots), n_slots};
+  CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.k1counters), 0, n_units * sizeof(unsigned int), s));
   K1Out o{ws_at<double>(ws, w.sigma2), nullptr, ws_at<float2>(ws, w.coef),
-          plan->k1_per_chunk ? ws_at<double2>(ws, w.block_bins) : nullptr,
+          ws_at<double>(ws, w.k1parts), ws_at<unsigned int>(ws, w.k1counters),
           K1_NOISE | K1_MMSE | K1_AI};
-  int rc = launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem,
-                     plan->k1_per_chunk, s);
+  int rc = launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem, s);
   if (rc) return rc;
   if (sigma2_hat)
     CUDA_TRY(cudaMemcpyAsync(sigma2_hat, ws_at<double>(ws, w.sigma2), n_units * sizeof(double),
@@ -519,19 +526,18 @@ extern "C" int arches_expert_from_ls(const arches_plan* plan, int32_t n_units, i
   const WsLayout w = ws_layout(plan, n_units);
   const float2* l = reinterpret_cast<const float2*>(ls);
   int rc;
+  CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.k1counters), 0, n_units * sizeof(unsigned int), s));
   if (which == 2) {
     LsFullSrc src{l};
-    K1Out o{nullptr, nullptr, ws_at<float2>(ws, w.coef), nullptr, K1_AI};
-    rc = launch_k1(plan, n_units, src, o, plan->dev.N, plan->k1_full_chunk, plan->k1_full_smem,
-                   false, s);
+    K1Out o{nullptr, nullptr, ws_at<float2>(ws, w.coef), ws_at<double>(ws, w.k1parts),
+            ws_at<unsigned int>(ws, w.k1counters), K1_AI};
+    rc = launch_k1(plan, n_units, src, o, plan->dev.N, plan->k1_full_chunk, plan->k1_full_smem, s);
   } else {
     LsCombSrc src{l};
     K1Out o{sigma2_hat ? sigma2_hat : ws_at<double>(ws, w.sigma2), noise_var_in,
-            which == 1 ? ws_at<float2>(ws, w.coef) : nullptr,
-            plan->k1_per_chunk ? ws_at<double2>(ws, w.block_bins) : nullptr,
-            which == 1 ? (K1_NOISE | K1_MMSE) : K1_NOISE};
-    rc = launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem,
-                   plan->k1_per_chunk, s);
+            which == 1 ? ws_at<float2>(ws, w.coef) : nullptr, ws_at<double>(ws, w.k1parts),
+            ws_at<unsigned int>(ws, w.k1counters), which == 1 ? (K1_NOISE | K1_MMSE) : K1_NOISE};
+    rc = launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem, s);
   }
   if (rc || which == 0) return rc;
   dim3 grid((plan->dev.N + 127) / 128, n_units);

@@ -56,17 +56,17 @@ struct K1Out {
   double* sigma2;           // [u] (may be null)
   const double* nv_in;      // [u] override (>= 0) or null
   float2* coef;             // [u][coef_floats2]
-  double2* block_bins;      // [u][n_blocks][AD][8] scratch (per-chunk mode)
+  double* parts;            // [u][n_parts][2*AD*L + 2] partial bins + energy (fp64)
+  unsigned int* counters;   // [u] arrival counters (self re-arming)
   int what;
 };
 
 __device__ inline void solve8_gram(const PlanDev& P, double s, double2* K /*[8][8]*/) {
-  // K = Pd (Gamma Pd + s I)^-1, Gaussian elimination with partial pivoting on
+  // K = Pd (Gamma Pd + s I)^-1, Gauss-Jordan with partial pivoting on
   // X^T: rows of K are solutions of (Gamma Pd + s I)^T z = Pd_row.
   double2 a[8][16];
   for (int i = 0; i < 8; ++i)
     for (int j = 0; j < 8; ++j) {
-      // (Gamma Pd + sI)^T [i][j] = (Gamma Pd + sI)[j][i] = Gamma[j][i] p_i + s delta
       double2 g = P.gram[j * 8 + i];
       a[i][j] = make_double2(g.x * P.pdp[i] + (i == j ? s : 0.0), g.y * P.pdp[i]);
       a[i][8 + j] = make_double2(i == j ? P.pdp[i] : 0.0, 0.0);
@@ -97,120 +97,154 @@ __device__ inline void solve8_gram(const PlanDev& P, double s, double2* K /*[8][
       }
     }
   }
-  // solution Z = X^{-T} Pd  =>  K = Z^T
   for (int i = 0; i < 8; ++i)
     for (int j = 0; j < 8; ++j) K[j * 8 + i] = a[i][8 + j];
 }
 
-template <class Src, bool kPerChunk>
+// One CTA per (part, unit): part p covers points [p*chunk, (p+1)*chunk).
+// In blocked-MMSE plans chunk == pilots per MMSE block, so a part's l < 8
+// partial bins are that block's bins (up to the block-origin phase).
+template <class Src>
 __global__ void __launch_bounds__(ARCHES_K1_THREADS)
     k1_analyze(const PlanDev P, const Src src, const K1Out out, const int npts, const int chunk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int u = blockIdx.x;
+  __shared__ double s_e[ARCHES_K1_THREADS / 32];
+  __shared__ int s_flag;
+  __shared__ double s_sc;
+  const int part = blockIdx.x, n_parts = gridDim.x;
+  const int u = blockIdx.y;
   const int tid = threadIdx.x;
   const int AD = P.A * P.D;
   const int L = P.L;
-  const int n_ad_t = (AD + ARCHES_RA - 1) / ARCHES_RA;
   const int n_l_t = (L + ARCHES_RL - 1) / ARCHES_RL;
-  const int n_tiles = n_ad_t * n_l_t;
+  const int n_tiles = ((AD + ARCHES_RA - 1) / ARCHES_RA) * n_l_t;
   const int KS = max(1, ARCHES_K1_THREADS / n_tiles);
   const int tile = tid / KS, ks = tid - tile * KS;
   const bool active = tile < n_tiles;
   const int ad0 = (tile / n_l_t) * ARCHES_RA, l0 = (tile % n_l_t) * ARCHES_RL;
   const float2* wtab = Src::kComb ? P.wM : P.wN;
+  const size_t rec = 2 * (size_t)AD * L + 2;  // doubles per partial record
 
-  // smem carve: [hs: AD*chunk float2 | red: 256*RA*RL float2 (aliased)]
-  //             [bins: AD*L double2] [scratch doubles 64] [K 64 double2]
+  // smem: [hs: AD*chunk float2 | red: 256*RA*RL float2 (aliased)] [bins: AD*L double2]
   float2* hs = reinterpret_cast<float2*>(smem_raw);
   float2* red = hs;
   const size_t stage = max((size_t)AD * chunk, (size_t)ARCHES_K1_THREADS * ARCHES_RA * ARCHES_RL);
   double2* bins = reinterpret_cast<double2*>(hs + stage);
-  double* scr = reinterpret_cast<double*>(bins + (size_t)AD * L);
-  double2* Kmat = reinterpret_cast<double2*>(scr + 64);
+  double2* Kmat = bins + (size_t)AD * L;
 
-  for (int i = tid; i < AD * L; i += blockDim.x) bins[i] = make_double2(0.0, 0.0);
-
+  const int base = part * chunk;
+  const int len = min(chunk, npts - base);
+  // ---- LS of this part into smem (loads batched for memory-level parallelism)
+  float e32 = 0.f;
+  {
+    int ad = tid / chunk, jj = tid - ad * chunk;
+    const int step_ad = ARCHES_K1_THREADS / chunk, step_j = ARCHES_K1_THREADS - step_ad * chunk;
+    for (int e = tid; e < AD * chunk; e += 8 * ARCHES_K1_THREADS) {
+      float2 v[8];
+      int aa[8], jv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        aa[q] = ad;
+        jv[q] = jj;
+        const bool ok = (ad < AD) && (jj < len);
+        v[q] = ok ? src.load(P, u, ad, base + jj) : make_float2(0.f, 0.f);
+        ad += step_ad;
+        jj += step_j;
+        if (jj >= chunk) {
+          jj -= chunk;
+          ++ad;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (aa[q] < AD) {
+          hs[(size_t)aa[q] * chunk + jv[q]] = v[q];
+          e32 = fmaf(v[q].x, v[q].x, fmaf(v[q].y, v[q].y, e32));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- partial analysis bins: register tile RA x RL over a K-slice of points
   float2 acc[ARCHES_RA][ARCHES_RL];
 #pragma unroll
   for (int i = 0; i < ARCHES_RA; ++i)
 #pragma unroll
-    for (int j = 0; j < ARCHES_RL; ++j) acc[i][j] = make_float2(0.f, 0.f);
-  double energy = 0.0;
-
-  const int n_chunks = (npts + chunk - 1) / chunk;
-  for (int c = 0; c < n_chunks; ++c) {
-    const int base = c * chunk;
-    const int len = min(chunk, npts - base);
-    __syncthreads();  // hs reuse
-    float e32 = 0.f;
-    for (int e = tid; e < AD * chunk; e += blockDim.x) {
-      const int ad = e / chunk, j = e - ad * chunk;
-      float2 v = make_float2(0.f, 0.f);
-      if (j < len) v = src.load(P, u, ad, base + j);
-      hs[e] = v;
-      e32 = fmaf(v.x, v.x, fmaf(v.y, v.y, e32));
-    }
-    energy += (double)e32;
-    __syncthreads();
-    if (active) {
-      for (int j = ks; j < len; j += KS) {
-        const int pt = base + j;
-        const float2 w1 = __ldg(&wtab[pt]);
-        float2 w = __ldg(&wtab[(int)(((long long)l0 * pt) % npts)]);
-        float2 hv[ARCHES_RA];
-#pragma unroll
-        for (int i = 0; i < ARCHES_RA; ++i)
-          hv[i] = (ad0 + i < AD) ? hs[(ad0 + i) * chunk + j] : make_float2(0.f, 0.f);
-#pragma unroll
-        for (int l = 0; l < ARCHES_RL; ++l) {
-#pragma unroll
-          for (int i = 0; i < ARCHES_RA; ++i) cfma(acc[i][l], hv[i], w);
-          w = cmul(w, w1);
-        }
-      }
-    }
-    if (kPerChunk || c == n_chunks - 1) {
-      // reduce the K-slices of this chunk (or of everything) in fixed order, fp64
-      __syncthreads();  // red aliases hs
+    for (int q = 0; q < ARCHES_RL; ++q) acc[i][q] = make_float2(0.f, 0.f);
+  if (active && ks < len) {
+    int pt = base + ks;
+    int idx = (int)(((long long)l0 * pt) % npts);
+    const int step = (int)(((long long)l0 * KS) % npts);
+    for (int j = ks; j < len; j += KS) {
+      const float2 w1 = __ldg(&wtab[pt]);
+      float2 w = __ldg(&wtab[idx]);
+      float2 hv[ARCHES_RA];
 #pragma unroll
       for (int i = 0; i < ARCHES_RA; ++i)
+        hv[i] = (ad0 + i < AD) ? hs[(ad0 + i) * chunk + j] : make_float2(0.f, 0.f);
 #pragma unroll
-        for (int l = 0; l < ARCHES_RL; ++l) {
-          red[(size_t)tid * ARCHES_RA * ARCHES_RL + i * ARCHES_RL + l] = acc[i][l];
-          if (kPerChunk) acc[i][l] = make_float2(0.f, 0.f);
-        }
-      __syncthreads();
-      for (int o = tid; o < AD * L; o += blockDim.x) {
-        const int ad = o / L, l = o - ad * L;
-        const int t = (ad / ARCHES_RA) * n_l_t + l / ARCHES_RL;
-        const int slot = (ad % ARCHES_RA) * ARCHES_RL + (l % ARCHES_RL);
-        double sx = 0.0, sy = 0.0;
-        for (int k = 0; k < KS; ++k) {
-          const float2 v = red[(size_t)(t * KS + k) * ARCHES_RA * ARCHES_RL + slot];
-          sx += (double)v.x;
-          sy += (double)v.y;
-        }
-        bins[o].x += sx;
-        bins[o].y += sy;
-        if (kPerChunk && l < 8 && out.block_bins) {
-          // block-local bins: remove the phase of the block origin (m0 = base)
-          double sn, cs;
-          sincospi(-2.0 * (double)(((long long)l * base) % npts) / (double)npts, &sn, &cs);
-          out.block_bins[(((size_t)u * P.n_blocks + c) * AD + ad) * 8 + l] =
-              make_double2(sx * cs - sy * sn, sx * sn + sy * cs);
-        }
+      for (int q = 0; q < ARCHES_RL; ++q) {
+#pragma unroll
+        for (int i = 0; i < ARCHES_RA; ++i) cfma(acc[i][q], hv[i], w);
+        w = cmul(w, w1);
       }
-      __syncthreads();
+      pt += KS;
+      idx += step;
+      if (idx >= npts) idx -= npts;
     }
   }
-
-  // ---- energy reduction (fixed order)
-  energy = warp_sum(energy);
-  if ((tid & 31) == 0) scr[tid >> 5] = energy;
+  __syncthreads();  // red aliases hs
+#pragma unroll
+  for (int i = 0; i < ARCHES_RA; ++i)
+#pragma unroll
+    for (int q = 0; q < ARCHES_RL; ++q)
+      red[(size_t)tid * ARCHES_RA * ARCHES_RL + i * ARCHES_RL + q] = acc[i][q];
+  double en = warp_sum((double)e32);
+  if ((tid & 31) == 0) s_e[tid >> 5] = en;
+  __syncthreads();
+  double* my = out.parts + ((size_t)u * n_parts + part) * rec;
+  for (int o = tid; o < AD * L; o += blockDim.x) {
+    const int ad = o / L, l = o - ad * L;
+    const int t = (ad / ARCHES_RA) * n_l_t + l / ARCHES_RL;
+    const int slot = (ad % ARCHES_RA) * ARCHES_RL + (l % ARCHES_RL);
+    double sx = 0.0, sy = 0.0;
+    for (int kk = 0; kk < KS; ++kk) {
+      const float2 v = red[(size_t)(t * KS + kk) * ARCHES_RA * ARCHES_RL + slot];
+      sx += (double)v.x;
+      sy += (double)v.y;
+    }
+    my[2 * o] = sx;
+    my[2 * o + 1] = sy;
+  }
+  if (tid == 0) {
+    double e = 0.0;
+    for (int w = 0; w < ARCHES_K1_THREADS / 32; ++w) e += s_e[w];
+    my[rec - 2] = e;
+  }
+  // ---- the last CTA of the unit reduces the parts (part order) and finalises
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned int prev = atomicAdd(out.counters + u, 1u);
+    s_flag = (prev == (unsigned int)n_parts - 1);
+    if (s_flag) out.counters[u] = 0u;
+  }
+  __syncthreads();
+  if (!s_flag) return;
+  __threadfence();
+  const double* all = out.parts + (size_t)u * n_parts * rec;
+  for (int o = tid; o < AD * L; o += blockDim.x) {
+    double sx = 0.0, sy = 0.0;
+    for (int p = 0; p < n_parts; ++p) {
+      sx += all[p * rec + 2 * o];
+      sy += all[p * rec + 2 * o + 1];
+    }
+    bins[o] = make_double2(sx, sy);
+  }
   __syncthreads();
   if (tid == 0) {
     double e = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) e += scr[w];
+    for (int p = 0; p < n_parts; ++p) e += all[p * rec + rec - 2];
     double sg = 0.0;
     if (Src::kComb) {
       for (int ad = 0; ad < AD; ++ad)
@@ -223,12 +257,12 @@ __global__ void __launch_bounds__(ARCHES_K1_THREADS)
     if (out.sigma2) out.sigma2[u] = nvhat;
     double s = nvhat;
     if (out.nv_in && out.nv_in[u] >= 0.0) s = out.nv_in[u];
-    scr[32] = s + P.ridge;
+    s_sc = s + P.ridge;
     if ((out.what & K1_MMSE) && !P.diag) solve8_gram(P, s + P.ridge, Kmat);
   }
   __syncthreads();
   if (!out.coef) return;
-  const double s = scr[32];
+  const double s = s_sc;
   float2* cm = out.coef + (size_t)u * coef_floats2(P);
   float2* ca = cm + (size_t)AD * P.n_blocks * 8;
   if (out.what & K1_MMSE) {
@@ -245,8 +279,16 @@ __global__ void __launch_bounds__(ARCHES_K1_THREADS)
         const int ad = o / (nb * 8), r = o - ad * nb * 8, b = r >> 3, l = r & 7;
         double2 acc2 = make_double2(0.0, 0.0);
         for (int lp = 0; lp < 8; ++lp) {
-          const double2 bb = (nb == 1) ? bins[ad * L + lp]
-                                       : out.block_bins[(((size_t)u * nb + b) * AD + ad) * 8 + lp];
+          double2 bb;
+          if (nb == 1) {
+            bb = bins[ad * L + lp];
+          } else {
+            // block-local bins: part b's partial with the block-origin phase removed
+            const double* pr = all + (size_t)b * rec + 2 * (ad * L + lp);
+            double sn, cs;
+            sincospi(-2.0 * (double)(((long long)lp * b * chunk) % npts) / (double)npts, &sn, &cs);
+            bb = make_double2(pr[0] * cs - pr[1] * sn, pr[0] * sn + pr[1] * cs);
+          }
           const double2 t = zmul(Kmat[l * 8 + lp], bb);
           acc2.x += t.x;
           acc2.y += t.y;

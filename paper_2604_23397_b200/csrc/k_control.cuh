@@ -32,10 +32,7 @@ __device__ __host__ inline StateView state_view(void* base, int stream, int wind
 
 __device__ inline void queue_insert(PendingMsg* q, int32_t& n, PendingMsg m) {
   // stable insertion by time (list.sort(key=...) keeps arrival order on ties)
-  if (n >= ARCHES_MAX_PENDING) {  // drop the oldest-applied slot: cannot happen with sane configs
-    for (int i = 1; i < n; ++i) q[i - 1] = q[i];
-    --n;
-  }
+  if (n >= ARCHES_MAX_PENDING) queue_pop_front(q, n);  // overflow: drop the earliest entry
   int pos = n;
   while (pos > 0 && q[pos - 1].at_ns > m.at_ns) {
     q[pos] = q[pos - 1];
@@ -45,8 +42,11 @@ __device__ inline void queue_insert(PendingMsg* q, int32_t& n, PendingMsg m) {
   ++n;
 }
 
+// queues are kept canonical: entries at index >= n are zero (so the
+// sequential and warp-parallel scans leave byte-identical state)
 __device__ inline void queue_pop_front(PendingMsg* q, int32_t& n) {
   for (int i = 1; i < n; ++i) q[i - 1] = q[i];
+  q[n - 1] = PendingMsg{0, 0, 0};
   --n;
 }
 

@@ -26,6 +26,81 @@ __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
   return v;
 }
 
+// register-resident copy of a PendingMsg queue (static indexing only)
+struct RegQueue {
+  int64_t at[ARCHES_MAX_PENDING];
+  int32_t mode[ARCHES_MAX_PENDING];
+  int32_t trig[ARCHES_MAX_PENDING];
+  int32_t n;
+  __device__ __forceinline__ void load(const PendingMsg* q, int32_t cnt) {
+    n = cnt;
+#pragma unroll
+    for (int i = 0; i < ARCHES_MAX_PENDING; ++i) {
+      at[i] = q[i].at_ns;
+      mode[i] = q[i].mode;
+      trig[i] = q[i].trigger;
+    }
+  }
+  __device__ __forceinline__ void store(PendingMsg* q, int32_t& cnt) const {
+    cnt = n;
+#pragma unroll
+    for (int i = 0; i < ARCHES_MAX_PENDING; ++i) {
+      q[i].at_ns = at[i];
+      q[i].mode = mode[i];
+      q[i].trigger = trig[i];
+    }
+  }
+  __device__ __forceinline__ void pop() {
+#pragma unroll
+    for (int i = 0; i < ARCHES_MAX_PENDING - 1; ++i) {
+      at[i] = at[i + 1];
+      mode[i] = mode[i + 1];
+      trig[i] = trig[i + 1];
+    }
+    at[ARCHES_MAX_PENDING - 1] = 0;
+    mode[ARCHES_MAX_PENDING - 1] = 0;
+    trig[ARCHES_MAX_PENDING - 1] = 0;
+    --n;
+  }
+  // stable insert by time (same semantics as queue_insert)
+  __device__ __forceinline__ void insert(int64_t t, int32_t m, int32_t tr) {
+    if (n >= ARCHES_MAX_PENDING) pop();
+    int pos = n;
+#pragma unroll
+    for (int i = ARCHES_MAX_PENDING - 1; i >= 0; --i)
+      if (i < n && at[i] > t) pos = i;
+#pragma unroll
+    for (int i = ARCHES_MAX_PENDING - 1; i > 0; --i)
+      if (i > pos && i <= n) {
+        at[i] = at[i - 1];
+        mode[i] = mode[i - 1];
+        trig[i] = trig[i - 1];
+      }
+#pragma unroll
+    for (int i = 0; i < ARCHES_MAX_PENDING; ++i)
+      if (i == pos) {
+        at[i] = t;
+        mode[i] = m;
+        trig[i] = tr;
+      }
+    ++n;
+  }
+};
+
+__device__ __forceinline__ void log_msg_fast(arches_message* log, int cap, int stream, int& cnt,
+                                             int mode, int64_t decided, int64_t deliverable,
+                                             int trigger) {
+  if (log && cnt < cap) {
+    arches_message m;
+    m.decided_at_ns = decided;
+    m.deliverable_at_ns = deliverable;
+    m.mode = mode;
+    m.trigger = trigger;
+    log[(size_t)stream * cap + cnt] = m;
+  }
+  ++cnt;
+}
+
 __global__ void __launch_bounds__(32) k4_kpm_scan_warp(const PlanDev P, const K4Args a) {
   const int stream = blockIdx.x;
   const int lane = threadIdx.x;
@@ -40,49 +115,69 @@ __global__ void __launch_bounds__(32) k4_kpm_scan_warp(const PlanDev P, const K4
   const int64_t slot_ns = P.slot_ns;
   int s0 = 0;
   while (s0 < a.n_slots) {
-    // ---------------- 1. sequential control walk (lane 0)
+    // ---------------- 1. sequential control walk (lane 0, registers only)
+    unsigned int good_mask = 0u;
+    if (P.policy == ARCHES_POLICY_ORACLE) {
+      const int uu = stream * a.n_slots + s0 + lane;
+      const int g = (s0 + lane < a.n_slots && a.regime && a.regime[uu]) ? 1 : 0;
+      good_mask = __ballot_sync(0xffffffffu, g);
+    }
     if (lane == 0) {
       StreamState& st = s_st;
+      RegQueue pq, fq;
+      pq.load(st.pending, st.n_pending);
+      fq.load(st.forced, st.n_forced);
+      int mode = st.mode, last_msg = st.last_msg_mode, since = st.since_decision;
+      int tripped = st.tripped;
+      int64_t last_del = st.last_delivery_ns;
+      int cnt = a.msg_count ? a.msg_count[stream] : 0;
+      const int64_t nbase = st.next_slot;
       int j = 0, decide = 0;
-      for (; j < 32 && s0 + j < a.n_slots; ++j) {
-        const int64_t n = st.next_slot + j;
+      const int lim = min(32, a.n_slots - s0);
+      for (; j < lim; ++j) {
+        const int64_t n = nbase + j;
         const int64_t t0 = n * slot_ns;
         const int64_t cut = (P.exec_mode == ARCHES_EXEC_SELECTED_ONLY) ? t0 - slot_ns : t0;
-        while (st.n_pending > 0 && st.pending[0].at_ns <= cut) {
-          st.mode = st.pending[0].mode;
-          queue_pop_front(st.pending, st.n_pending);
+        while (pq.n > 0 && pq.at[0] <= cut) {
+          mode = pq.mode[0];
+          pq.pop();
         }
-        while (st.n_forced > 0 && st.forced[0].at_ns <= t0) {
-          st.mode = st.forced[0].mode;
-          queue_pop_front(st.forced, st.n_forced);
+        while (fq.n > 0 && fq.at[0] <= t0) {
+          mode = fq.mode[0];
+          fq.pop();
         }
-        s_mode[j] = st.mode;
-        const int64_t end_ns = (n + 1) * slot_ns;
+        s_mode[j] = mode;
+        const int64_t end_ns = t0 + slot_ns;
         if (P.policy == ARCHES_POLICY_ORACLE) {
-          const int u = stream * a.n_slots + s0 + j;
-          const int want = (a.regime && a.regime[u]) ? 1 : 0;
-          if (want != st.last_msg_mode) {
-            PendingMsg m = {end_ns, want, ARCHES_TRIGGER_ORACLE};
-            queue_insert(st.pending, st.n_pending, m);
-            st.last_msg_mode = want;
-            log_message(a.msg_log, a.msg_count, a.msg_cap, stream, want, end_ns, end_ns,
-                        ARCHES_TRIGGER_ORACLE);
+          const int want = (good_mask >> j) & 1;
+          if (want != last_msg) {
+            pq.insert(end_ns, want, ARCHES_TRIGGER_ORACLE);
+            last_msg = want;
+            log_msg_fast(a.msg_log, a.msg_cap, stream, cnt, want, end_ns, end_ns,
+                         ARCHES_TRIGGER_ORACLE);
           }
         } else if (P.policy == ARCHES_POLICY_TREE) {
-          if (++st.since_decision >= P.decision_period) {
+          if (++since >= P.decision_period) {
             decide = 1;  // features of slots <= n needed: stop the walk here
             ++j;
             break;
           }
-          if (!st.tripped && end_ns - st.last_delivery_ns > P.failsafe_timeout_ns && st.mode != 1) {
-            st.tripped = 1;
-            PendingMsg f = {end_ns, 1, ARCHES_TRIGGER_FAILSAFE};
-            queue_insert(st.forced, st.n_forced, f);
-            log_message(a.msg_log, a.msg_count, a.msg_cap, stream, 1, end_ns, end_ns,
-                        ARCHES_TRIGGER_FAILSAFE);
+          if (!tripped && end_ns - last_del > P.failsafe_timeout_ns && mode != 1) {
+            tripped = 1;
+            fq.insert(end_ns, 1, ARCHES_TRIGGER_FAILSAFE);
+            log_msg_fast(a.msg_log, a.msg_cap, stream, cnt, 1, end_ns, end_ns,
+                         ARCHES_TRIGGER_FAILSAFE);
           }
         }
       }
+      pq.store(st.pending, st.n_pending);
+      fq.store(st.forced, st.n_forced);
+      st.mode = mode;
+      st.last_msg_mode = last_msg;
+      st.since_decision = since;
+      st.tripped = tripped;
+      st.last_delivery_ns = last_del;
+      if (a.msg_count) a.msg_count[stream] = cnt;
       s_len = j;
       s_decide = decide;
     }

@@ -138,13 +138,19 @@ struct K2Args {
 };
 
 // NE experts held per thread: 2 = pipeline (MMSE, AI synthesised),
-// 1 = compat (estimate loaded from args.est)
+// 1 = compat (estimate loaded from args.est).
+// The CTA's y tile (A*T rows) and tx tile (T rows) of 128 subcarriers are
+// staged into shared memory by cp.async.bulk (TMA) at entry, so the whole
+// tile is in flight while the expert synthesis runs.
 template <int NA, int ND, int NE>
 __global__ void __launch_bounds__(ARCHES_TILE)
     k2_synth_equalize(const PlanDev P, const K2Args args) {
-  // dynamic smem: [s_cm: nbt_max][AD*8] rotated MMSE taps, [s_ca: AD*trunc] rotated AI taps
-  extern __shared__ __align__(16) float2 s_dyn[];
+  // dynamic smem: [y tile A*T*TILE][tx tile T*TILE][s_cm nbt_max*AD*8][s_ca AD*trunc]
+  extern __shared__ __align__(128) float2 s_dyn[];
   __shared__ double s_scr[11 * (ARCHES_TILE / 32)];
+  __shared__ float s_tw[ARCHES_MAX_SYM][ND];
+  __shared__ int s_dm[ARCHES_MAX_SYM];
+  __shared__ __align__(8) uint64_t s_bar;
   __shared__ int s_flag;
   const int u = blockIdx.y;
   const int tile = blockIdx.x;
@@ -154,11 +160,41 @@ __global__ void __launch_bounds__(ARCHES_TILE)
   const bool valid = k < P.N;
   const int AD = P.A * ND;  // runtime antennas (<= NA, padded lanes masked)
   const int T = P.T;
+  const int ncol = min(ARCHES_TILE, P.N - k0);
+
+  float2* s_y = s_dyn;
+  float2* s_x = s_y + (size_t)P.A * T * ARCHES_TILE;
+  float2* s_cm = s_x + (size_t)T * ARCHES_TILE;
+  float2* s_ca = s_cm + (size_t)P.nbt_max * AD * 8;
+
+  // ---- issue the tile copies (warp 0), TMA completes on s_bar
+  if (j == 0) mbar_init(&s_bar, 1);
+  if (j < T) {
+    for (int d = 0; d < ND; ++d) s_tw[j][d] = P.tw[j][d];
+    s_dm[j] = P.is_dmrs[j];
+  }
+  __syncthreads();
+  if (j < 32) {
+    const uint32_t rowb = (uint32_t)ncol * sizeof(float2);
+    const int rows = P.A * T + T;
+    if (j == 0) mbar_arrive_expect_tx(&s_bar, rowb * rows);
+    __syncwarp();
+    const uint64_t pol = l2_evict_first_policy();
+    for (int r = j; r < rows; r += 32) {
+      const float2* src;
+      float2* dst;
+      if (r < P.A * T) {
+        src = args.y + ((size_t)u * P.A * T + r) * P.N + k0;
+        dst = s_y + (size_t)r * ARCHES_TILE;
+      } else {
+        src = args.tx + ((size_t)u * T + (r - P.A * T)) * P.N + k0;
+        dst = s_x + (size_t)(r - P.A * T) * ARCHES_TILE;
+      }
+      bulk_g2s(dst, src, rowb, &s_bar, pol);
+    }
+  }
 
   float2 h[NE][NA][ND];
-  float2* s_cm = s_dyn;
-  float2* s_ca = s_dyn + (size_t)P.nbt_max * AD * 8;
-
   if (NE == 2) {
     // ---- stage rotated coefficients: c'_l = c_l e^{-2 pi i l (k0 - origin)/N}
     const float2* cm = args.coef + (size_t)u * coef_floats2(P);
@@ -230,6 +266,7 @@ __global__ void __launch_bounds__(ARCHES_TILE)
   double v[11];
 #pragma unroll
   for (int i = 0; i < 11; ++i) v[i] = 0.0;
+  mbar_wait(&s_bar, 0);  // y / tx tile resident
   if (valid) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
@@ -247,19 +284,17 @@ __global__ void __launch_bounds__(ARCHES_TILE)
     }
     // ---- equaliser: interpolate in time, MRC over antennas, SINR sums in fp64
     const float nv = (float)args.nv[u];
-    const size_t yb = (size_t)u * P.A * T * P.N + k;
-    const size_t xb = (size_t)u * T * P.N + k;
     const bool even = (k & 1) == 0;
     for (int t = 0; t < T; ++t) {
       float2 yv[NA];
 #pragma unroll
       for (int a = 0; a < NA; ++a)
-        yv[a] = (a < P.A) ? __ldg(&args.y[yb + ((size_t)a * T + t) * P.N]) : make_float2(0.f, 0.f);
-      const float2 x = __ldg(&args.tx[xb + (size_t)t * P.N]);
-      const bool data = !(even && P.is_dmrs[t] >= 0);
+        yv[a] = (a < P.A) ? s_y[((size_t)a * T + t) * ARCHES_TILE + j] : make_float2(0.f, 0.f);
+      const float2 x = s_x[(size_t)t * ARCHES_TILE + j];
+      const bool data = !(even && s_dm[t] >= 0);
       float wt[ND];
 #pragma unroll
-      for (int d = 0; d < ND; ++d) wt[d] = (d == P.tw_d0[t]) ? P.tw_w0[t] : ((d == P.tw_d1[t]) ? P.tw_w1[t] : 0.f);
+      for (int d = 0; d < ND; ++d) wt[d] = s_tw[t][d];
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
         float2 num = make_float2(0.f, 0.f);
@@ -278,7 +313,7 @@ __global__ void __launch_bounds__(ARCHES_TILE)
         }
         const float inv = 1.0f / (den + nv);
         const float2 xh = make_float2(num.x * inv, num.y * inv);
-        if (args.x_hat) args.x_hat[xb + (size_t)t * P.N] = xh;
+        if (args.x_hat) args.x_hat[((size_t)u * T + t) * P.N + k] = xh;
         if (data) {
           const double xr = x.x, xi = x.y, hr = xh.x, hi = xh.y;
           v[5 + e] += xr * hr + xi * hi;   // Re conj(x) xh
