@@ -30,6 +30,14 @@ __device__ __host__ inline StateView state_view(void* base, int stream, int wind
   return v;
 }
 
+// queues are kept canonical: entries at index >= n are zero (so the
+// sequential and warp-parallel scans leave byte-identical state)
+__device__ inline void queue_pop_front(PendingMsg* q, int32_t& n) {
+  for (int i = 1; i < n; ++i) q[i - 1] = q[i];
+  q[n - 1] = PendingMsg{0, 0, 0};
+  --n;
+}
+
 __device__ inline void queue_insert(PendingMsg* q, int32_t& n, PendingMsg m) {
   // stable insertion by time (list.sort(key=...) keeps arrival order on ties)
   if (n >= ARCHES_MAX_PENDING) queue_pop_front(q, n);  // overflow: drop the earliest entry
@@ -42,13 +50,7 @@ __device__ inline void queue_insert(PendingMsg* q, int32_t& n, PendingMsg m) {
   ++n;
 }
 
-// queues are kept canonical: entries at index >= n are zero (so the
-// sequential and warp-parallel scans leave byte-identical state)
-__device__ inline void queue_pop_front(PendingMsg* q, int32_t& n) {
-  for (int i = 1; i < n; ++i) q[i - 1] = q[i];
-  q[n - 1] = PendingMsg{0, 0, 0};
-  --n;
-}
+
 
 // ThroughputWindow.push (phy_pipeline.py:334-340) with the ring indexed by push
 // count n (ring[n % W] holds the value pushed W slots ago until overwritten)
