@@ -241,7 +241,7 @@ def run_ours(a, rank, world, dist):
     for r in range(reps):
         ev[4 * r].record()
         _lib.check(L.arches_ls_analyze(plan.handle, 1, S, _lib.ptr(eng.y), _lib.ptr(eng.pilots),
-                                       None, _lib.ptr(ws), st))
+                                       None, -1, _lib.ptr(eng.state), None, _lib.ptr(ws), st))
         ev[4 * r + 1].record()
         _lib.check(L.arches_experts_equalize(plan.handle, 1, S, _lib.ptr(eng.y), _lib.ptr(eng.tx),
                                              _lib.ptr(eng.noise_var), _lib.ptr(eng.seeds), -1,

@@ -173,9 +173,13 @@ int arches_state_init(const arches_plan* plan, void* state, int32_t n_streams,
  * Replaces ls_estimate (expert_bank.py:96-116), estimate_noise_var (:199-214)
  * and the noise-dependent half of mmse_estimate/_wiener_matrix (:139-177) and
  * denoiser_estimate (:182-196): comb Y/X, 20-bin comb DFT, Parseval tail
- * power -> sigma2_hat, per-unit Wiener taps and AI taps (written to ws). */
+ * power -> sigma2_hat, per-unit Wiener taps and AI taps (written to ws).
+ * When seeds != NULL the last CTA of each unit also draws the unit's Philox
+ * CRC uniform and LCID4 split (rng.py:24-34, phy_pipeline.py:221,347-350) for
+ * run_batch's K2; slot numbering as in arches_experts_equalize. */
 int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
-                      const void* y, const void* pilots, double* sigma2_hat, void* ws,
+                      const void* y, const void* pilots, const uint64_t* seeds,
+                      int64_t first_slot, const void* state, double* sigma2_hat, void* ws,
                       arches_stream_t stream);
 
 /* ---- K2: expert synthesis + switch telemetry + equaliser ------------

@@ -4,9 +4,12 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <complex>
 #include <vector>
 
@@ -15,6 +18,7 @@
 #include "k_control.cuh"
 #include "k_control_warp.cuh"
 #include "k_synth_eq.cuh"
+#include "k_synth_tc.cuh"
 #include "rng.cuh"
 
 #define ARCHES_VERSION "arches-b200 0.1 (sm_100a)"
@@ -56,14 +60,30 @@ struct arches_plan {
   int k1_full_parts;
   size_t k1_full_smem;
   size_t k2_smem;
+  size_t k2_tc_smem;  // 0: tensor-core K2 not applicable to this plan
   void* dev_tables;
 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// cudaFuncSetAttribute is a synchronous host call: do it once per kernel (to the
+// largest value requested so far) so eager launches stay back-to-back.
+template <typename K>
+static cudaError_t ensure_smem(K kern, size_t smem) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> set_to;  // per kernel function
+  if (smem <= 48 * 1024) return cudaSuccess;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = set_to[reinterpret_cast<const void*>(kern)];
+  if (smem <= cur) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
+
 // ------------------------------------------------------------ workspace
 struct WsLayout {
-  size_t coef, parts, counters, k1parts, k1counters, sigma2, total;
+  size_t coef, parts, counters, k1parts, k1counters, sigma2, rng, total;
 };
 
 static WsLayout ws_layout(const arches_plan* P, int n_units) {
@@ -85,6 +105,8 @@ static WsLayout ws_layout(const arches_plan* P, int n_units) {
   off += align256((size_t)n_units * sizeof(unsigned int));
   w.sigma2 = off;
   off += align256((size_t)n_units * sizeof(double));
+  w.rng = off;
+  off += align256((size_t)n_units * 2 * sizeof(double));
   w.total = off;
   return w;
 }
@@ -258,10 +280,49 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
       }
       gram[l * 8 + lp] = make_double2(re, im);
     }
-  const size_t off_wN = align256(M * sizeof(float2));
-  const size_t off_syn = off_wN + align256(N * sizeof(float2));
-  const size_t off_gram = off_syn + align256(syn.size() * sizeof(float2));
-  const size_t total = off_gram + align256(64 * sizeof(double2));
+  // K2 tensor-core operand S[j][kappa] (j < 128, kappa = 2l + c): per row j,
+  // per 8-wide K block c: 8 tf32 "hi" values then the 8 matching "lo" values
+  // (round-to-nearest split), ready for tcgen05.st into the row's TMEM lane.
+  const int lsyn = ((std::max(p.truncation, 8) + 3) / 4) * 4;
+  d.tc_kb = lsyn / 4;
+  const size_t row_words = (size_t)d.tc_kb * 16;
+  std::vector<float> atab((size_t)ARCHES_TILE * row_words, 0.f);
+  auto tf32 = [](float x) {
+    uint32_t b;
+    memcpy(&b, &x, 4);
+    b = (b + 0x1000u) & 0xFFFFE000u;  // round to nearest (ties away), 10-bit mantissa
+    float r;
+    memcpy(&r, &b, 4);
+    return r;
+  };
+  for (int j = 0; j < ARCHES_TILE; ++j)
+    for (int kap = 0; kap < 2 * lsyn; ++kap) {
+      const int l = kap >> 1;
+      const long long idx = ((long long)l * j) % N;
+      const double ang = -2.0 * M_PI * (double)idx / (double)N;
+      const float x = (float)((kap & 1) ? sin(ang) : cos(ang));
+      const float hi = tf32(x), lo = tf32(x - hi);
+      const size_t o = (size_t)j * row_words + (size_t)(kap >> 3) * 16 + (kap & 7);
+      atab[o] = hi;
+      atab[o + 8] = lo;
+    }
+  // per-tile synthesis rotations (fp64 -> fp32): AI e^{-2 pi i l k0/N} (l < Lsyn),
+  // MMSE e^{-2 pi i l (k0 - b block)/N} (l < 8)
+  const int rstride = lsyn + 8;
+  std::vector<float2> rot((size_t)d.n_tiles * rstride);
+  for (int t = 0; t < d.n_tiles; ++t) {
+    const int k0 = t * ARCHES_TILE;
+    const int b = std::min(k0 / block, d.n_blocks - 1);
+    for (int l = 0; l < rstride; ++l) {
+      const long long off = l < lsyn ? (long long)l * k0 : (long long)(l - lsyn) * (k0 - b * block);
+      const long long idx = ((off % N) + N) % N;
+      const double a = -2.0 * M_PI * (double)idx / (double)N;
+      rot[(size_t)t * rstride + l] = make_float2((float)cos(a), (float)sin(a));
+    }
+  }
+  const size_t off_tca = off_gram + align256(64 * sizeof(double2));
+  const size_t off_rot = off_tca + align256(atab.size() * sizeof(float));
+  const size_t total = off_rot + align256(rot.size() * sizeof(float2));
   unsigned char* buf = nullptr;
   cudaError_t err = cudaMalloc(&buf, total);
   if (err != cudaSuccess) {
@@ -271,6 +332,8 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
   cudaMemcpy(buf, wM.data(), M * sizeof(float2), cudaMemcpyHostToDevice);
   cudaMemcpy(buf + off_wN, wN.data(), N * sizeof(float2), cudaMemcpyHostToDevice);
   cudaMemcpy(buf + off_syn, syn.data(), syn.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  cudaMemcpy(buf + off_tca, atab.data(), atab.size() * sizeof(float), cudaMemcpyHostToDevice);
+  cudaMemcpy(buf + off_rot, rot.data(), rot.size() * sizeof(float2), cudaMemcpyHostToDevice);
   err = cudaMemcpy(buf + off_gram, gram.data(), 64 * sizeof(double2), cudaMemcpyHostToDevice);
   if (err != cudaSuccess) {
     cudaFree(buf);
@@ -282,6 +345,14 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
   d.wN = reinterpret_cast<const float2*>(buf + off_wN);
   d.syn = reinterpret_cast<const float2*>(buf + off_syn);
   d.gram = reinterpret_cast<const double2*>(buf + off_gram);
+  d.tc_a = reinterpret_cast<const float*>(buf + off_tca);
+  d.tc_rot = reinterpret_cast<const float2*>(buf + off_rot);
+  {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    d.num_sms = sms > 0 ? sms : 148;
+  }
 
   // ---- K1 launch geometry
   const int AD = d.A * d.D;
@@ -299,6 +370,18 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
   P->k1_full_smem = k1_smem(P->k1_full_chunk);
   P->k2_smem = ((size_t)(d.A + 1) * d.T * ARCHES_TILE + (size_t)d.nbt_max * AD * 8 +
                 (size_t)AD * d.trunc) * sizeof(float2);
+  {
+    // tcgen05 K2: n_ant in {1,2,4} (padded), tiles inside one MMSE block
+    const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : d.A <= 4 ? 4 : 0;
+    const bool tile_ok = d.n_blocks == 1 || (d.block % ARCHES_TILE) == 0;
+    size_t sm = 0;
+    if (na && tile_ok && 16 * d.tc_kb + 4 * na * d.D <= 128 && !getenv("ARCHES_DISABLE_TC")) {
+      const int R = 2 * na * d.D, ncol = ((2 * R + 15) / 16) * 16, ng = ncol / 8;
+      sm = (size_t)(d.A + 1) * d.T * ARCHES_TILE * sizeof(float2) + 2 * (size_t)d.tc_kb * ng * 256;
+      if (sm > 227 * 1024) sm = 0;
+    }
+    P->k2_tc_smem = sm;
+  }
   if (P->k2_smem > 200 * 1024) {
     cudaFree(buf);
     delete P;
@@ -340,7 +423,7 @@ template <class Src>
 static int launch_k1(const arches_plan* P, int n_units, const Src& src, const K1Out& o, int npts,
                      int chunk, size_t smem, cudaStream_t s) {
   auto kern = k1_analyze<Src>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(ensure_smem(kern, smem));
   dim3 grid((npts + chunk - 1) / chunk, n_units);
   kern<<<grid, ARCHES_K1_THREADS, smem, s>>>(P->dev, src, o, npts, chunk);
   LAUNCH_CHECK();
@@ -348,8 +431,9 @@ static int launch_k1(const arches_plan* P, int n_units, const Src& src, const K1
 }
 
 extern "C" int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
-                                 const void* y, const void* pilots, double* sigma2_hat, void* ws,
-                                 arches_stream_t stream) {
+                                 const void* y, const void* pilots, const uint64_t* seeds,
+                                 int64_t first_slot, const void* state, double* sigma2_hat,
+                                 void* ws, arches_stream_t stream) {
   if (!plan || !y || !pilots || !ws || n_streams < 1 || n_slots < 1)
     return set_err(ARCHES_E_CONTRACT, "bad ls_analyze args");
   const int n_units = n_streams * n_slots;
@@ -357,9 +441,13 @@ extern "C" int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int
   const WsLayout w = ws_layout(plan, n_units);
   GridCombSrc src{reinterpret_cast<const float2*>(y), reinterpret_cast<const float2*>(pilots), n_slots};
   CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.k1counters), 0, n_units * sizeof(unsigned int), s));
+  if (seeds && first_slot < 0 && !state)
+    return set_err(ARCHES_E_CONTRACT, "first_slot < 0 needs the stream state (slot source)");
   K1Out o{ws_at<double>(ws, w.sigma2), nullptr, ws_at<float2>(ws, w.coef),
           ws_at<double>(ws, w.k1parts), ws_at<unsigned int>(ws, w.k1counters),
-          K1_NOISE | K1_MMSE | K1_AI};
+          K1_NOISE | K1_MMSE | K1_AI, seeds ? ws_at<double>(ws, w.rng) : nullptr, seeds,
+          reinterpret_cast<const unsigned char*>(state),
+          state_stride_bytes(plan->dev.window_length, plan->dev.dapp_window), first_slot, n_slots};
   int rc = launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem, s);
   if (rc) return rc;
   if (sigma2_hat)
@@ -379,7 +467,7 @@ static int launch_k2(const arches_plan* P, int n_units, const K2Args& a, cudaStr
 #define K2_CASE(NA_, ND_)                                                                   \
   if (na == NA_ && d.D == ND_) {                                                            \
     auto kern = k2_synth_equalize<NA_, ND_, NE>;                                            \
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    CUDA_TRY(ensure_smem(kern, smem)); \
     kern<<<grid, ARCHES_TILE, smem, s>>>(d, a);                                             \
     LAUNCH_CHECK();                                                                         \
     return ARCHES_OK;                                                                       \
@@ -392,11 +480,54 @@ static int launch_k2(const arches_plan* P, int n_units, const K2Args& a, cudaStr
   return set_err(ARCHES_E_CONFIG, "unsupported (n_ant, n_dmrs) = (%d, %d)", d.A, d.D);
 }
 
+static int experts_equalize_impl(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                                 const void* y, const void* tx, const double* noise_var,
+                                 const uint64_t* seeds, int64_t first_slot, const void* state,
+                                 void* h_mmse, void* h_ai, arches_telemetry* tel, void* ws,
+                                 arches_stream_t stream, bool rng_from_k1);
+
+static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cudaStream_t s) {
+  const PlanDev& d = P->dev;
+  const int n_items = n_units * d.n_tiles;
+  const dim3 grid(d.n_tiles, n_units);
+  const size_t smem = P->k2_tc_smem;
+  const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : 4;
+  const bool std_pat = d.T == 14 && d.D == 3 && d.dsym[0] == 0 && d.dsym[1] == 5 && d.dsym[2] == 10;
+#define K2TC_LAUNCH(NA_, ND_, STD_)                                                          \
+  {                                                                                          \
+    auto kern = k2_tc<NA_, ND_, STD_>;                                                       \
+    CUDA_TRY(ensure_smem(kern, smem)); \
+    kern<<<grid, TC_THREADS, smem, s>>>(d, a, n_items);                                      \
+    LAUNCH_CHECK();                                                                          \
+    return ARCHES_OK;                                                                        \
+  }
+#define K2TC_CASE(NA_, ND_)                                                                  \
+  if (na == NA_ && d.D == ND_) K2TC_LAUNCH(NA_, ND_, false)
+  if (std_pat && na == 4) K2TC_LAUNCH(4, 3, true)
+  if (std_pat && na == 2) K2TC_LAUNCH(2, 3, true)
+  if (std_pat && na == 1) K2TC_LAUNCH(1, 3, true)
+  K2TC_CASE(1, 1) K2TC_CASE(1, 2) K2TC_CASE(1, 3) K2TC_CASE(1, 4)
+  K2TC_CASE(2, 1) K2TC_CASE(2, 2) K2TC_CASE(2, 3) K2TC_CASE(2, 4)
+  K2TC_CASE(4, 1) K2TC_CASE(4, 2) K2TC_CASE(4, 3) K2TC_CASE(4, 4)
+#undef K2TC_CASE
+#undef K2TC_LAUNCH
+  return launch_k2<2>(P, n_units, a, s);
+}
+
 extern "C" int arches_experts_equalize(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                                        const void* y, const void* tx, const double* noise_var,
                                        const uint64_t* seeds, int64_t first_slot,
                                        const void* state, void* h_mmse, void* h_ai,
                                        arches_telemetry* tel, void* ws, arches_stream_t stream) {
+  return experts_equalize_impl(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
+                               state, h_mmse, h_ai, tel, ws, stream, false);
+}
+
+static int experts_equalize_impl(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                                 const void* y, const void* tx, const double* noise_var,
+                                 const uint64_t* seeds, int64_t first_slot, const void* state,
+                                 void* h_mmse, void* h_ai, arches_telemetry* tel, void* ws,
+                                 arches_stream_t stream, bool rng_from_k1) {
   if (!plan || !y || !tx || !noise_var || !seeds || !ws || !tel || n_streams < 1 || n_slots < 1)
     return set_err(ARCHES_E_CONTRACT, "bad experts_equalize args");
   if (first_slot < 0 && !state)
@@ -422,6 +553,8 @@ extern "C" int arches_experts_equalize(const arches_plan* plan, int32_t n_stream
   a.state_stride = state_stride_bytes(plan->dev.window_length, plan->dev.dapp_window);
   a.first_slot = first_slot;
   a.n_slots = n_slots;
+  a.rng = rng_from_k1 ? ws_at<double>(ws, w.rng) : nullptr;
+  if (plan->k2_tc_smem) return launch_k2_tc(plan, n_units, a, s);
   return launch_k2<2>(plan, n_units, a, s);
 }
 
@@ -470,10 +603,11 @@ extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int3
                                 void* h_mmse, void* h_ai, arches_telemetry* tel, arches_kpm* kpm,
                                 arches_message* msg_log, int32_t* msg_count, int32_t msg_cap,
                                 void* ws, arches_stream_t stream) {
-  int rc = arches_ls_analyze(plan, n_streams, n_slots, y, pilots, nullptr, ws, stream);
+  int rc = arches_ls_analyze(plan, n_streams, n_slots, y, pilots, seeds, first_slot, state,
+                             nullptr, ws, stream);
   if (rc) return rc;
-  rc = arches_experts_equalize(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
-                               state, h_mmse, h_ai, tel, ws, stream);
+  rc = experts_equalize_impl(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
+                             state, h_mmse, h_ai, tel, ws, stream, true);
   if (rc) return rc;
   return arches_kpm_scan(plan, n_streams, n_slots, tel, regime, tree, state, kpm, msg_log,
                          msg_count, msg_cap, stream);
@@ -530,13 +664,14 @@ extern "C" int arches_expert_from_ls(const arches_plan* plan, int32_t n_units, i
   if (which == 2) {
     LsFullSrc src{l};
     K1Out o{nullptr, nullptr, ws_at<float2>(ws, w.coef), ws_at<double>(ws, w.k1parts),
-            ws_at<unsigned int>(ws, w.k1counters), K1_AI};
+            ws_at<unsigned int>(ws, w.k1counters), K1_AI, nullptr, nullptr, nullptr, 0, 0, 1};
     rc = launch_k1(plan, n_units, src, o, plan->dev.N, plan->k1_full_chunk, plan->k1_full_smem, s);
   } else {
     LsCombSrc src{l};
     K1Out o{sigma2_hat ? sigma2_hat : ws_at<double>(ws, w.sigma2), noise_var_in,
             which == 1 ? ws_at<float2>(ws, w.coef) : nullptr, ws_at<double>(ws, w.k1parts),
-            ws_at<unsigned int>(ws, w.k1counters), which == 1 ? (K1_NOISE | K1_MMSE) : K1_NOISE};
+            ws_at<unsigned int>(ws, w.k1counters), which == 1 ? (K1_NOISE | K1_MMSE) : K1_NOISE,
+            nullptr, nullptr, nullptr, 0, 0, 1};
     rc = launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem, s);
   }
   if (rc || which == 0) return rc;

@@ -31,6 +31,10 @@ struct PlanDev {
   const float2* wN;             // [N] e^{+2 pi i j / N}
   const float2* syn;            // [L][TILE] e^{-2 pi i l j / N}
   const double2* gram;          // [8][8] F^H F of one MMSE block
+  const float* tc_a;            // K2 tensor-core synthesis operand (UMMA layout, hi | lo)
+  int tc_kb;                    // its 8-wide K blocks (Lsyn / 4)
+  const float2* tc_rot;         // [n_tiles][4*tc_kb + 8]: e^{-2 pi i l k0/N} (AI), e^{-2 pi i l (k0-b*block)/N} (MMSE)
+  int num_sms;
   // KPM layer
   double sinr_cap_db, lcid4_fraction, lcid4_jitter, crc_margin_db, crc_scale_db;
   double slot_us, slot_s;
@@ -49,7 +53,8 @@ struct PlanDev {
 //   cm[ad][b][8]  MMSE synthesis taps per block (float2)
 //   ca[ad][T]     AI synthesis taps (float2)
 __host__ __device__ inline size_t coef_floats2(const PlanDev& P) {
-  return (size_t)P.A * P.D * (P.n_blocks * 8 + P.trunc);
+  const size_t n = (size_t)P.A * P.D * (P.n_blocks * 8 + P.trunc);
+  return (n + 1) & ~(size_t)1;  // 16-byte multiple (bulk-copy granule)
 }
 
 // K2 per-tile partial sums (fp64), reduced in tile order by the last CTA.
@@ -130,12 +135,14 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  // try_wait with a suspend-time hint: the waiting warp sleeps instead of
+  // spinning on issue slots the compute warps need
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(phase)
+      "r"(phase), "r"(0x10000u)
       : "memory");
 }
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {

@@ -15,6 +15,7 @@
 // from an exactly rounded table plus a <= 4-step recurrence.
 #pragma once
 #include "common.cuh"
+#include "rng.cuh"
 
 // --- point sources -------------------------------------------------------
 // pipeline: comb REs of the received grid divided by the pilots
@@ -59,6 +60,13 @@ struct K1Out {
   double* parts;            // [u][n_parts][2*AD*L + 2] partial bins + energy (fp64)
   unsigned int* counters;   // [u] arrival counters (self re-arming)
   int what;
+  // per-unit RNG side products for K2 (Philox CRC uniform, LCID4 split)
+  double* rng;              // [u][2] or null
+  const uint64_t* seeds;    // [stream]
+  const unsigned char* state;
+  size_t state_stride;
+  long long first_slot;     // < 0: stream next_slot from state
+  int n_slots;
 };
 
 __device__ inline void solve8_gram(const PlanDev& P, double s, double2* K /*[8][8]*/) {
@@ -242,6 +250,17 @@ __global__ void __launch_bounds__(ARCHES_K1_THREADS)
     bins[o] = make_double2(sx, sy);
   }
   __syncthreads();
+  if (tid == 32 && out.rng) {  // RNG side products (independent of the bins: other warp)
+    const int stream = u / out.n_slots;
+    const long long base = out.first_slot >= 0
+        ? out.first_slot
+        : (long long)*reinterpret_cast<const int64_t*>(out.state + (size_t)stream * out.state_stride);
+    const long long slot = base + (u - stream * out.n_slots);
+    out.rng[2 * u] = arches_rng::stream_first_uniform(out.seeds[stream], P.crc_key, (uint64_t)slot);
+    const double j = arches_rng::lcid4_jitter((uint64_t)slot);
+    const double f = __dadd_rn(P.lcid4_fraction, __dmul_rn(P.lcid4_jitter, j));
+    out.rng[2 * u + 1] = fmin(fmax(f, 0.0), 1.0);
+  }
   if (tid == 0) {
     double e = 0.0;
     for (int p = 0; p < n_parts; ++p) e += all[p * rec + rec - 2];

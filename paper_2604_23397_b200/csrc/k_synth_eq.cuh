@@ -58,7 +58,8 @@ __device__ inline double lcid4_frac(const PlanDev& P, long long slot) {
 // last-CTA finalisation: reduce partials (tile order) and fill the telemetry
 __device__ inline void finalize_unit(const PlanDev& P, const TilePartial* parts, int n_tiles,
                                      const double* sigma2, uint64_t seed, long long slot,
-                                     int n_experts, arches_telemetry* tel) {
+                                     int n_experts, arches_telemetry* tel,
+                                     const double* rng = nullptr) {
   double acc[11];
   for (int i = 0; i < 11; ++i) acc[i] = 0.0;
   for (int t = 0; t < n_tiles; ++t) {
@@ -68,8 +69,9 @@ __device__ inline void finalize_unit(const PlanDev& P, const TilePartial* parts,
   const double cnt = (double)P.A * P.D * P.N;
   arches_telemetry out;
   out.sigma2_hat = sigma2 ? *sigma2 : 0.0;
-  const double u_crc = arches_rng::stream_first_uniform(seed, P.crc_key, (uint64_t)slot);
-  const double frac = lcid4_frac(P, slot);
+  // Philox CRC uniform and LCID4 split: precomputed by K1 when available
+  const double u_crc = rng ? rng[0] : arches_rng::stream_first_uniform(seed, P.crc_key, (uint64_t)slot);
+  const double frac = rng ? rng[1] : lcid4_frac(P, slot);
   for (int e = 0; e < 2; ++e) {
     const int src = (n_experts == 2) ? e : 0;
     out.abs_mean[e] = acc[0 + src] / cnt;
@@ -131,6 +133,7 @@ struct K2Args {
   double* sinr_out;       // compat: [u] sinr / abs_mean / rsrp of expert 0
   double* abs_out;
   double* rsrp_out;
+  const double* rng;            // [u][2] (u_crc, lcid4 frac) from K1, or null
   const unsigned char* state;  // per-stream control state (next_slot at offset 0)
   size_t state_stride;
   long long first_slot;         // < 0: take each stream's next_slot from `state`
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(ARCHES_TILE)
     arches_telemetry tel;
     finalize_unit(P, args.parts + (size_t)u * gridDim.x, gridDim.x,
                   args.sigma2 ? args.sigma2 + u : nullptr, args.seeds ? args.seeds[stream] : 0ull,
-                  slot, NE, &tel);
+                  slot, NE, &tel, args.rng ? args.rng + 2 * u : nullptr);
     if (args.tel) args.tel[u] = tel;
     if (args.sinr_out) args.sinr_out[u] = tel.sinr_db[0];
     if (args.abs_out) args.abs_out[u] = tel.abs_mean[0];
