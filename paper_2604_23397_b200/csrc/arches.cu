@@ -320,6 +320,9 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
       rot[(size_t)t * rstride + l] = make_float2((float)cos(a), (float)sin(a));
     }
   }
+  const size_t off_wN = align256(M * sizeof(float2));
+  const size_t off_syn = off_wN + align256(N * sizeof(float2));
+  const size_t off_gram = off_syn + align256(syn.size() * sizeof(float2));
   const size_t off_tca = off_gram + align256(64 * sizeof(double2));
   const size_t off_rot = off_tca + align256(atab.size() * sizeof(float));
   const size_t total = off_rot + align256(rot.size() * sizeof(float2));
