@@ -355,6 +355,8 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     d.num_sms = sms > 0 ? sms : 148;
+    const char* pf = getenv("ARCHES_K2_PREFETCH");
+    d.pf_dist = pf ? atoi(pf) : 0;
   }
 
   // ---- K1 launch geometry
@@ -378,10 +380,11 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
     const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : d.A <= 4 ? 4 : 0;
     const bool tile_ok = d.n_blocks == 1 || (d.block % ARCHES_TILE) == 0;
     size_t sm = 0;
-    if (na && tile_ok && 16 * d.tc_kb + 4 * na * d.D <= 128 && !getenv("ARCHES_DISABLE_TC")) {
+    if (na && tile_ok && 16 * d.tc_kb <= 128 && !getenv("ARCHES_DISABLE_TC")) {
       const int R = 2 * na * d.D, ncol = ((2 * R + 15) / 16) * 16, ng = ncol / 8;
-      sm = (size_t)(d.A + 1) * d.T * ARCHES_TILE * sizeof(float2) + 2 * (size_t)d.tc_kb * ng * 256;
-      if (sm > 227 * 1024) sm = 0;
+      const int n_b = (ncol / 2) * 4 * d.tc_kb;  // B entries: <= 2 per thread of 512
+      sm = 2 * (size_t)(d.A + 1) * d.T * ARCHES_TILE * sizeof(float2) + 4 * (size_t)d.tc_kb * ng * 256;
+      if (sm > 227 * 1024 || n_b > 2 * TC_THREADS || ncol > 64) sm = 0;
     }
     P->k2_tc_smem = sm;
   }
@@ -492,7 +495,7 @@ static int experts_equalize_impl(const arches_plan* plan, int32_t n_streams, int
 static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cudaStream_t s) {
   const PlanDev& d = P->dev;
   const int n_items = n_units * d.n_tiles;
-  const dim3 grid(d.n_tiles, n_units);
+  const int grid = std::min(n_items, d.num_sms);  // persistent: one CTA per SM
   const size_t smem = P->k2_tc_smem;
   const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : 4;
   const bool std_pat = d.T == 14 && d.D == 3 && d.dsym[0] == 0 && d.dsym[1] == 5 && d.dsym[2] == 10;
@@ -502,13 +505,15 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
     CUDA_TRY(ensure_smem(kern, smem)); \
     kern<<<grid, TC_THREADS, smem, s>>>(d, a, n_items);                                      \
     LAUNCH_CHECK();                                                                          \
+    k3_finalize<<<(n_units + 127) / 128, 128, 0, s>>>(d, a, n_units);                        \
+    LAUNCH_CHECK();                                                                          \
     return ARCHES_OK;                                                                        \
   }
 #define K2TC_CASE(NA_, ND_)                                                                  \
   if (na == NA_ && d.D == ND_) K2TC_LAUNCH(NA_, ND_, false)
-  if (std_pat && na == 4) K2TC_LAUNCH(4, 3, true)
-  if (std_pat && na == 2) K2TC_LAUNCH(2, 3, true)
-  if (std_pat && na == 1) K2TC_LAUNCH(1, 3, true)
+  if (std_pat && d.A == 4) K2TC_LAUNCH(4, 3, true)  /* kStd: exact n_ant, NR 0/5/10 pattern */
+  if (std_pat && d.A == 2) K2TC_LAUNCH(2, 3, true)
+  if (std_pat && d.A == 1) K2TC_LAUNCH(1, 3, true)
   K2TC_CASE(1, 1) K2TC_CASE(1, 2) K2TC_CASE(1, 3) K2TC_CASE(1, 4)
   K2TC_CASE(2, 1) K2TC_CASE(2, 2) K2TC_CASE(2, 3) K2TC_CASE(2, 4)
   K2TC_CASE(4, 1) K2TC_CASE(4, 2) K2TC_CASE(4, 3) K2TC_CASE(4, 4)

@@ -35,6 +35,7 @@ struct PlanDev {
   int tc_kb;                    // its 8-wide K blocks (Lsyn / 4)
   const float2* tc_rot;         // [n_tiles][4*tc_kb + 8]: e^{-2 pi i l k0/N} (AI), e^{-2 pi i l (k0-b*block)/N} (MMSE)
   int num_sms;
+  int pf_dist;                  // K2 L2 prefetch distance in CTAs (0 = off)
   // KPM layer
   double sinr_cap_db, lcid4_fraction, lcid4_jitter, crc_margin_db, crc_scale_db;
   double slot_us, slot_s;
@@ -154,6 +155,9 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {

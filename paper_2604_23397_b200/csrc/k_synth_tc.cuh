@@ -1,23 +1,26 @@
 // K2 (tensor-core form) -- expert synthesis on tcgen05 + switch telemetry +
-// equaliser.  One CTA (8 warps) per (unit, 128-subcarrier tile):
-//   * warp 0 issues cp.async.bulk (TMA) copies of the tile's y (A*T rows) and
-//     tx (T rows) into shared memory at entry; they land while the synthesis runs;
-//   * warps 0..3 write their TMEM lanes' rows of the twiddle operand
-//     S[j][2l] = cos(-2 pi l j/N), S[j][2l+1] = sin(-2 pi l j/N) (hi | lo split,
-//     from a pre-split plan table) with tcgen05.st -- A operand in TMEM;
-//   * all threads build B, the real embedding of both experts' complex taps
-//     rotated to the tile origin (hi | lo), in shared memory (UMMA K-major);
-//   * one thread issues D[128 x 4AD] = S_hi B_hi + S_lo B_hi + S_hi B_lo
-//     (tcgen05.mma kind::tf32, A from TMEM, fp32-accurate 3xTF32) and commits;
-//   * thread = (subcarrier j = TMEM lane, expert = warp / 4): tcgen05.ld of its
-//     expert's taps, output stores, |H| telemetry, time interpolation + MRC
-//     equaliser (compile-time weights for the NR 0/5/10 pattern), fp32
-//     per-thread SINR partial sums reduced in fp64, last-CTA finalisation.
+// equaliser, persistent and software-pipelined: one CTA of 16 warps per SM
+// loops over work items (unit, 128-subcarrier tile).  Iteration i:
+//   * thread 0 issues the cp.async.bulk (TMA) copies of item i+1's y / tx rows
+//     into the other shared-memory stage (double buffer), so HBM streams while
+//     item i is equalised;
+//   * every thread pulls its share of item i+1's coefficients (L2) early;
+//   * thread (subcarrier j = TMEM lane, expert = warp/4 & 1, symbol half =
+//     warp/8) reads item i's synthesised taps from TMEM (tcgen05.ld), stores
+//     the expert outputs + |H| telemetry (half 0), and equalises its half of the
+//     symbols from the stage (compile-time weights for the NR 0/5/10 pattern);
+//   * then B(i+1) -- both experts' taps rotated to the tile origin, real
+//     embedding, hi | lo -- is written to shared memory, one __syncthreads, and
+//     thread 0 issues D(i+1) = S_hi B_hi + S_lo B_hi + S_hi B_lo
+//     (tcgen05.mma kind::tf32, A = twiddles S in TMEM, 3xTF32) into the other
+//     TMEM accumulator; it completes while item i+1's data lands.
+// Per-tile partial sums are reduced in a fixed order (fp32 per thread, fp64
+// across threads); the last tile of a unit finalises its telemetry.
 #pragma once
 #include "common.cuh"
 #include "k_synth_eq.cuh"
 
-#define TC_THREADS 256
+#define TC_THREADS 512
 
 __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   // SWIZZLE_NONE K-major canonical layout: core matrices of 8 rows x 16 B,
@@ -153,7 +156,9 @@ __device__ __forceinline__ void eq_re(const float2 (&h)[NA][ND], const float* wt
     num.y = fmaf(hn.x, yv[a].y, fmaf(-hn.y, yv[a].x, num.y));
     den = fmaf(hn.x, hn.x, fmaf(hn.y, hn.y, den));
   }
-  const float inv = __frcp_rn(den + nv) * m;  // m = 0 on pilot REs
+  float inv;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(den + nv));
+  inv *= m;  // m = 0 on pilot REs
   const float hr = num.x * inv, hi = num.y * inv;
   sre = fmaf(x.x, hr, fmaf(x.y, hi, sre));
   sim = fmaf(x.x, hi, fmaf(-x.y, hr, sim));
@@ -182,42 +187,81 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, u
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
 }
 
-// TMEM columns: [0, 4KB) S_hi, [4KB, 8KB) S_lo ... rounded: A_hi at 0, A_lo at 64 - 8KB? keep simple:
-//   S_hi  cols [0, 8*KB)      S_lo cols [8*KB, 16*KB)      D cols [16*KB, 16*KB + NCOL)
+// this thread's <= 2 B entries (output column pair r, tap l), fixed per thread
+struct BEntry {
+  int r, l;
+};
+
+template <int NA, int ND>
+__device__ __forceinline__ void load_b_entries(const PlanDev& P, const float2* coef_u, int tile,
+                                               const BEntry (&be)[2], float2 (&cv)[2]) {
+  constexpr int R = 2 * NA * ND;
+  const int L4 = 4 * P.tc_kb;
+  const int AD = P.A * ND;
+  const float2* cm = coef_u;
+  const float2* ca = cm + (size_t)AD * P.n_blocks * 8;
+  const float2* rot = P.tc_rot + (size_t)tile * (L4 + 8);
+  const int b = P.n_blocks == 1 ? 0 : min(tile * ARCHES_TILE / P.block, P.n_blocks - 1);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int r = be[q].r, l = be[q].l;
+    float2 c = make_float2(0.f, 0.f);
+    if (r < NA * ND) {
+      if (r < AD && l < P.trunc) c = cmul(__ldg(&ca[r * P.trunc + l]), __ldg(&rot[l]));
+    } else if (r < R) {
+      const int ad = r - NA * ND;
+      if (ad < AD && l < 8)
+        c = cmul(__ldg(&cm[((size_t)ad * P.n_blocks + b) * 8 + l]), __ldg(&rot[L4 + l]));
+    }
+    cv[q] = c;
+  }
+}
+
 template <int NA, int ND, bool kStd>
-__global__ void __launch_bounds__(TC_THREADS)
+__global__ void __launch_bounds__(TC_THREADS, 1)
     k2_tc(const PlanDev P, const K2Args args, const int n_items) {
   constexpr int R = 2 * NA * ND;                    // complex outputs: AI then MMSE
   constexpr int NCOL = ((2 * R + 15) / 16) * 16;    // MMA N (real columns)
   constexpr int NG = NCOL / 8;
   constexpr int CPE = 2 * NA * ND;                  // D columns per expert
   extern __shared__ __align__(128) unsigned char sm[];
-  __shared__ __align__(8) uint64_t s_bar[2];        // [0] y/tx landed, [1] MMA done
+  __shared__ __align__(8) uint64_t s_full[2];       // stage landed
+  __shared__ __align__(8) uint64_t s_mma[2];        // accumulator ready
   __shared__ uint32_t s_tmem;
-  __shared__ double s_red[11][8];
-  __shared__ int s_flag;
-  const int KB = P.tc_kb;
+  __shared__ double s_red[2][11][8];
+  const int KB = P.tc_kb, L4 = 4 * KB;
   const int T = P.T;
+  const int TH = (T + 1) >> 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ex = warp >> 2;                         // expert of this warp: 0 = AI, 1 = MMSE
   const int q4 = warp & 3;                          // TMEM lane quarter
+  const int ex = (warp >> 2) & 1;                   // expert: 0 = AI, 1 = MMSE
+  const int half = warp >> 3;                       // symbol half
   const int j = q4 * 32 + lane;                     // subcarrier within the tile = TMEM lane
-  const int u = blockIdx.y, tile = blockIdx.x;
-  const int k0 = tile * ARCHES_TILE;
-  const int kk = k0 + j;
-  const bool valid = kk < P.N;
-  const int ncol = min(ARCHES_TILE, P.N - k0);
   const int AD = P.A * ND;
+  const int n_tiles = P.n_tiles;
+  const int G = gridDim.x;
   const uint32_t b_bytes = (uint32_t)KB * NG * 256;
-  float2* sYX = reinterpret_cast<float2*>(sm);                      // [(A+1)*T][TILE]
-  unsigned char* sB = sm + (size_t)(P.A + 1) * T * ARCHES_TILE * sizeof(float2);  // [hi | lo]
+  const size_t stage_elems = (size_t)(P.A + 1) * T * ARCHES_TILE;
+  float2* sYX = reinterpret_cast<float2*>(sm);                               // [2][stage]
+  unsigned char* sB = sm + 2 * stage_elems * sizeof(float2);                 // [2][hi | lo]
+  const int n_all = (NCOL / 2) * L4;                                         // B entries
+  const uint32_t ACC0 = 128;                                                 // TMEM columns
+  BEntry be[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int e = threadIdx.x + q * TC_THREADS;
+    be[q].r = e < n_all ? e / L4 : (1 << 20);  // out of range -> zero, skipped
+    be[q].l = e < n_all ? e - be[q].r * L4 : 0;
+  }
 
   if (threadIdx.x == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
+    mbar_init(&s_mma[0], 1);
+    mbar_init(&s_mma[1], 1);
   }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
         smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -225,83 +269,30 @@ __global__ void __launch_bounds__(TC_THREADS)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  // ---- y / tx tile -> shared memory (TMA), in flight during the synthesis
-  if (warp == 0) {
-    const uint32_t rowb = (uint32_t)ncol * sizeof(float2);
+  const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
+
+  auto issue_tma = [&](int item, int stage) {  // warp 0 (lanes split the rows)
+    const int u = item / n_tiles, tile = item - u * n_tiles, k0 = tile * ARCHES_TILE;
+    const uint32_t rowb = (uint32_t)min(ARCHES_TILE, P.N - k0) * sizeof(float2);
     const int rows = (P.A + 1) * T;
-    if (lane == 0) mbar_arrive_expect_tx(&s_bar[0], rowb * rows);
+    if (lane == 0) mbar_arrive_expect_tx(&s_full[stage], rowb * rows);
     __syncwarp();
     const uint64_t pol = l2_evict_first_policy();
+    float2* dst = sYX + (size_t)stage * stage_elems;
     for (int r = lane; r < rows; r += 32) {
       const float2* src = (r < P.A * T) ? args.y + ((size_t)u * P.A * T + r) * P.N + k0
                                         : args.tx + ((size_t)u * T + (r - P.A * T)) * P.N + k0;
-      bulk_g2s(sYX + (size_t)r * ARCHES_TILE, src, rowb, &s_bar[0], pol);
+      bulk_g2s(dst + (size_t)r * ARCHES_TILE, src, rowb, &s_full[stage], pol);
     }
-  }
-  // ---- A operand rows (this lane's subcarrier) -> TMEM, from the pre-split table
-  if (ex == 0) {
-    const float4* arow = reinterpret_cast<const float4*>(P.tc_a) + (size_t)j * (KB * 4);  // 16*KB floats
-    const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
-    for (int c = 0; c < KB; ++c) {  // 16 floats per step: 8 hi (cols 8c..) + 8 lo
-      float v[16];
+  };
+  auto write_b = [&](int buf, const float2* cv) {  // this thread's <= 2 entries
+    unsigned char* bhi = sB + (size_t)buf * 2 * b_bytes;
+    unsigned char* blo = bhi + b_bytes;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4 f = __ldg(&arow[c * 4 + i]);
-        v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
-      }
-      // v[0..7] = S_hi[j][8c .. 8c+7], v[8..15] = S_lo[j][8c .. 8c+7]
-      float hi8[16], lo8[16];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) { hi8[i] = v[i]; lo8[i] = v[8 + i]; }
-#pragma unroll
-      for (int i = 8; i < 16; ++i) { hi8[i] = 0.f; lo8[i] = 0.f; }
-      (void)hi8; (void)lo8;
-      // store as two x8 groups: hi at column 8c, lo at column 8KB + 8c
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                       lane_base + 8 * c),
-                   "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-                   "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-                   "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
-                   : "memory");
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                       lane_base + 8 * KB + 8 * c),
-                   "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
-                   "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
-                   "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
-                   : "memory");
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  }
-  // ---- B operand: both experts' taps rotated to the tile origin (hi | lo)
-  {
-    for (uint32_t i = threadIdx.x; i < 2 * b_bytes / 4; i += blockDim.x)
-      reinterpret_cast<float*>(sB)[i] = 0.f;
-    __syncthreads();
-    const float2* cm = args.coef + (size_t)u * coef_floats2(P);
-    const float2* ca = cm + (size_t)AD * P.n_blocks * 8;
-    const int rstride = 4 * KB + 8;
-    const float2* rot = P.tc_rot + (size_t)tile * rstride;
-    const int b = min(k0 / P.block, P.n_blocks - 1);
-    unsigned char* bhi = sB;
-    unsigned char* blo = sB + b_bytes;
-    const int n_ai = AD * P.trunc, n_all = n_ai + AD * 8;
-    for (int e = threadIdx.x; e < n_all; e += blockDim.x) {
-      int r, l;
-      float2 c, w;
-      if (e < n_ai) {
-        const int ad = e / P.trunc;
-        l = e - ad * P.trunc;
-        r = ad;
-        c = __ldg(&ca[e]);
-        w = __ldg(&rot[l]);
-      } else {
-        const int e2 = e - n_ai, ad = e2 >> 3;
-        l = e2 & 7;
-        r = NA * ND + ad;
-        c = __ldg(&cm[((size_t)ad * P.n_blocks + b) * 8 + l]);
-        w = __ldg(&rot[4 * KB + l]);
-      }
-      c = cmul(c, w);
+    for (int q = 0; q < 2; ++q) {
+      if (be[q].r >= (1 << 20)) break;
+      const int r = be[q].r, l = be[q].l;
+      const float2 c = cv[q];
       const float rh = tf32_rna(c.x), rl = tf32_rna(c.x - rh);
       const float ih = tf32_rna(c.y), il = tf32_rna(c.y - ih);
       const uint32_t o0 = kmaj_off(2 * r, 2 * l, NG), o1 = kmaj_off(2 * r + 1, 2 * l, NG);
@@ -311,133 +302,209 @@ __global__ void __launch_bounds__(TC_THREADS)
       *reinterpret_cast<float2*>(blo + o1) = make_float2(il, rl);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  // ---- MMA: D = S_hi B_hi + S_lo B_hi + S_hi B_lo
-  const uint32_t d_col = 16u * KB;
-  if (threadIdx.x == 0) {
+  };
+  auto issue_mma = [&](int buf) {  // thread 0 only, after a CTA barrier
     tc_fence_after();
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NCOL >> 3) << 17) |
                            ((uint32_t)(ARCHES_TILE >> 4) << 24);
-    const uint32_t b_hi = smem_u32(sB), b_lo = b_hi + b_bytes;
+    const uint32_t b_hi = smem_u32(sB + (size_t)buf * 2 * b_bytes), b_lo = b_hi + b_bytes;
+    const uint32_t dcol = tmem + ACC0 + 64u * buf;
     for (int kb = 0; kb < KB; ++kb) {
       const uint64_t dbh = umma_desc_kmajor(b_hi + kb * NG * 256, 128, 256);
       const uint64_t dbl = umma_desc_kmajor(b_lo + kb * NG * 256, 128, 256);
       const uint32_t ah = tmem + 8u * kb, al = tmem + 8u * KB + 8u * kb;
-      umma_tf32_ts(tmem + d_col, ah, dbh, idesc, kb > 0 ? 1u : 0u);
-      umma_tf32_ts(tmem + d_col, al, dbh, idesc, 1u);
-      umma_tf32_ts(tmem + d_col, ah, dbl, idesc, 1u);
+      umma_tf32_ts(dcol, ah, dbh, idesc, kb > 0 ? 1u : 0u);
+      umma_tf32_ts(dcol, al, dbh, idesc, 1u);
+      umma_tf32_ts(dcol, ah, dbl, idesc, 1u);
     }
-    umma_commit(&s_bar[1]);
+    umma_commit(&s_mma[buf]);
+  };
+
+  const int first = blockIdx.x;
+  // ---- prologue: A operand (twiddle rows) -> TMEM, item 0 data + B(0) + MMA(0)
+  if (first < n_items) {
+    if (warp == 0) issue_tma(first, 0);
+    if (warp < 4) {
+      const float4* arow = reinterpret_cast<const float4*>(P.tc_a) + (size_t)j * (KB * 4);
+      for (int c = 0; c < KB; ++c) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 f = __ldg(&arow[c * 4 + i]);
+          v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+        }
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                         lane_base + 8 * c),
+                     "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                     "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                     "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+                     : "memory");
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                         lane_base + 8 * KB + 8 * c),
+                     "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+                     "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+                     "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    float2 cv[2];
+    const int u0 = first / n_tiles;
+    load_b_entries<NA, ND>(P, args.coef + (size_t)u0 * coef_floats2(P), first - u0 * n_tiles, be, cv);
+    write_b(0, cv);
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) issue_mma(0);
   }
-  // ---- this thread's expert taps
-  mbar_wait(&s_bar[1], 0);
-  tc_fence_after();
-  float vals[CPE];
-  tmem_ld_n<CPE>(tmem + ((uint32_t)(q4 * 32) << 16) + d_col + (uint32_t)(ex * CPE), vals);
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-  float2 h[NA][ND];
-#pragma unroll
-  for (int a = 0; a < NA; ++a)
-#pragma unroll
-    for (int d = 0; d < ND; ++d)
-      h[a][d] = make_float2(vals[2 * (a * ND + d)], vals[2 * (a * ND + d) + 1]);
-  float sa = 0.f, sp = 0.f, sre = 0.f, sim = 0.f, syy = 0.f, sxx = 0.f;
-  float2* hout = ex ? args.h_mmse : args.h_ai;
-  if (valid) {
-    if (hout) {
-      const size_t ob = (size_t)u * AD * P.N + kk;
-#pragma unroll
-      for (int a = 0; a < NA; ++a)
-        if (a < P.A)
-#pragma unroll
-          for (int d = 0; d < ND; ++d) hout[ob + (size_t)(a * ND + d) * P.N] = h[a][d];
+
+  for (int i = 0;; ++i) {
+    const int item = first + i * G;
+    if (item >= n_items) break;
+    const int buf = i & 1, ph = (i >> 1) & 1;
+    const int nxt = item + G;
+    const bool has_next = nxt < n_items;
+    const int u = item / n_tiles, tile = item - u * n_tiles;
+    const int k0 = tile * ARCHES_TILE;
+    const int kk = k0 + j;
+    const bool valid = kk < P.N;
+    // ---- next item's data + coefficients in flight during this item's work
+    if (has_next && warp == 0) issue_tma(nxt, buf ^ 1);
+    float2 cv[2];
+    if (has_next) {
+      const int un = nxt / n_tiles;
+      load_b_entries<NA, ND>(P, args.coef + (size_t)un * coef_floats2(P), nxt - un * n_tiles, be, cv);
     }
+    const float nv = (float)__ldg(&args.nv[u]);
+    // ---- this expert's synthesised taps
+    mbar_wait(&s_mma[buf], ph);
+    tc_fence_after();
+    float vals[CPE];
+    tmem_ld_n<CPE>(lane_base + ACC0 + 64u * buf + (uint32_t)(ex * CPE), vals);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float2 h[NA][ND];
 #pragma unroll
     for (int a = 0; a < NA; ++a)
 #pragma unroll
-      for (int d = 0; d < ND; ++d) {
-        const float p2 = fmaf(h[a][d].x, h[a][d].x, h[a][d].y * h[a][d].y);
-        sa += sqrtf(p2);
-        sp += p2;
-      }
-  }
-  // ---- equaliser from the staged tile
-  mbar_wait(&s_bar[0], 0);
-  if (valid) {
-    const float nv = (float)__ldg(&args.nv[u]);
-    const float modd = (kk & 1) ? 1.f : 0.f;  // pilot REs: even k on DMRS symbols
-    const float2* yrow = sYX + j;
-    const float2* xrow = sYX + (size_t)P.A * T * ARCHES_TILE + j;
-    if (kStd) {
+      for (int d = 0; d < ND; ++d)
+        h[a][d] = make_float2(vals[2 * (a * ND + d)], vals[2 * (a * ND + d) + 1]);
+    float sa = 0.f, sp = 0.f, sre = 0.f, sim = 0.f, syy = 0.f, sxx = 0.f;
+    float2* hout = ex ? args.h_mmse : args.h_ai;
+    if (valid && half == 0 && hout) {  // half 0 stores the expert output ...
+      float2* o = hout + (size_t)u * AD * P.N + kk;
 #pragma unroll
-      for (int t = 0; t < 14; ++t) {
-        float wt[ND];
+      for (int a = 0; a < NA; ++a)
+        if (kStd || a < P.A)
 #pragma unroll
-        for (int d = 0; d < ND; ++d) wt[d] = std_tw(t, d);
-        float2 yv[NA];
+          for (int d = 0; d < ND; ++d) o[(size_t)(a * ND + d) * P.N] = h[a][d];
+    }
+    if (valid && half == 1) {  // ... half 1 forms its |H| telemetry
 #pragma unroll
-        for (int a = 0; a < NA; ++a)
-          yv[a] = (a < P.A) ? yrow[(size_t)(a * 14 + t) * ARCHES_TILE] : make_float2(0.f, 0.f);
-        const float2 x = xrow[(size_t)t * ARCHES_TILE];
-        const float m = (t == 0 || t == 5 || t == 10) ? modd : 1.f;
-        eq_re<NA, ND>(h, wt, yv, x, m, nv, sre, sim, syy);
-        if (ex == 0) sxx = fmaf(m * x.x, x.x, fmaf(m * x.y, x.y, sxx));
-      }
-    } else {
-      for (int t = 0; t < T; ++t) {
-        float wt[ND];
+      for (int a = 0; a < NA; ++a)
 #pragma unroll
-        for (int d = 0; d < ND; ++d) wt[d] = P.tw[t][d];
-        float2 yv[NA];
+        for (int d = 0; d < ND; ++d) {
+          const float p2 = fmaf(h[a][d].x, h[a][d].x, h[a][d].y * h[a][d].y);
+          sa += sqrtf(p2);
+          sp += p2;
+        }
+    }
+    // ---- equaliser over this thread's symbol half
+    mbar_wait(&s_full[buf], ph);
+    if (valid) {
+      const float modd = (kk & 1) ? 1.f : 0.f;  // pilot REs: even k on DMRS symbols
+      const float2* yrow = sYX + (size_t)buf * stage_elems + j;
+      const float2* xrow = yrow + (size_t)P.A * T * ARCHES_TILE;
+      if (kStd) {
 #pragma unroll
-        for (int a = 0; a < NA; ++a)
-          yv[a] = (a < P.A) ? yrow[(size_t)(a * T + t) * ARCHES_TILE] : make_float2(0.f, 0.f);
-        const float2 x = xrow[(size_t)t * ARCHES_TILE];
-        const float m = (P.is_dmrs[t] >= 0) ? modd : 1.f;
-        eq_re<NA, ND>(h, wt, yv, x, m, nv, sre, sim, syy);
-        if (ex == 0) sxx = fmaf(m * x.x, x.x, fmaf(m * x.y, x.y, sxx));
+        for (int tt = 0; tt < 7; ++tt) {
+          const int t = half * 7 + tt;
+          float wt[ND];
+#pragma unroll
+          for (int d = 0; d < ND; ++d) wt[d] = half ? std_tw(7 + tt, d) : std_tw(tt, d);
+          float2 yv[NA];  // kStd plans have n_ant == NA exactly
+#pragma unroll
+          for (int a = 0; a < NA; ++a) yv[a] = yrow[(size_t)(a * 14 + t) * ARCHES_TILE];
+          const float2 x = xrow[(size_t)t * ARCHES_TILE];
+          const bool dm = half ? (7 + tt == 10) : (tt == 0 || tt == 5);
+          const float m = dm ? modd : 1.f;
+          eq_re<NA, ND>(h, wt, yv, x, m, nv, sre, sim, syy);
+          if (ex == 0) sxx = fmaf(m * x.x, x.x, fmaf(m * x.y, x.y, sxx));
+        }
+      } else {
+        const int t0 = half ? TH : 0, t1 = half ? T : TH;
+        for (int t = t0; t < t1; ++t) {
+          float wt[ND];
+#pragma unroll
+          for (int d = 0; d < ND; ++d) wt[d] = P.tw[t][d];
+          float2 yv[NA];
+#pragma unroll
+          for (int a = 0; a < NA; ++a)
+            yv[a] = (a < P.A) ? yrow[(size_t)(a * T + t) * ARCHES_TILE] : make_float2(0.f, 0.f);
+          const float2 x = xrow[(size_t)t * ARCHES_TILE];
+          const float m = (P.is_dmrs[t] >= 0) ? modd : 1.f;
+          eq_re<NA, ND>(h, wt, yv, x, m, nv, sre, sim, syy);
+          if (ex == 0) sxx = fmaf(m * x.x, x.x, fmaf(m * x.y, x.y, sxx));
+        }
       }
     }
-  }
-  // ---- tile partials (fixed order) + last-CTA finalisation
-  {
-    const double r0 = warp_sum((double)sa), r1 = warp_sum((double)sp);
-    const double r2 = warp_sum((double)sre), r3 = warp_sum((double)sim);
-    const double r4 = warp_sum((double)syy), r5 = warp_sum((double)sxx);
-    if (lane == 0) {
-      for (int i = 0; i < 11; ++i) s_red[i][warp] = 0.0;
-      s_red[0 + ex][warp] = r0;
-      s_red[2 + ex][warp] = r1;
-      s_red[4][warp] = r5;
-      s_red[5 + ex][warp] = r2;
-      s_red[7 + ex][warp] = r3;
-      s_red[9 + ex][warp] = r4;
+    // ---- per-warp partials -> s_red[buf] (column = half*4 + quarter order)
+    {
+      const int col = half * 4 + (q4 ^ 0);
+      const double r2 = warp_sum((double)sre), r3 = warp_sum((double)sim);
+      const double r4 = warp_sum((double)syy);
+      double r0 = 0.0, r1 = 0.0, r5 = 0.0;
+      if (half == 1) {
+        r0 = warp_sum((double)sa);
+        r1 = warp_sum((double)sp);
+      }
+      if (ex == 0) r5 = warp_sum((double)sxx);
+      if (lane == 0) {
+        if (half == 1) {
+          s_red[buf][0 + ex][q4] = r0;
+          s_red[buf][2 + ex][q4] = r1;
+        }
+        if (ex == 0) s_red[buf][4][col] = r5;
+        s_red[buf][5 + ex][col] = r2;
+        s_red[buf][7 + ex][col] = r3;
+        s_red[buf][9 + ex][col] = r4;
+      }
+    }
+    // ---- B(i+1) -> shared memory, one barrier, MMA(i+1)
+    if (has_next) write_b(buf ^ 1, cv);
+    tc_fence_before();
+    __syncthreads();
+    if (has_next && threadIdx.x == 0) issue_mma(buf ^ 1);
+    // ---- tile partial (fixed order); per-unit finalisation runs in K3
+    if (warp == 1 && lane < 11) {
+      double acc;
+      if (lane < 4) {  // abs / pow: half 1 only
+        acc = ((s_red[buf][lane][0] + s_red[buf][lane][1]) + s_red[buf][lane][2]) + s_red[buf][lane][3];
+      } else {
+        acc = 0.0;
+        for (int w = 0; w < 8; ++w) acc += s_red[buf][lane][w];
+      }
+      reinterpret_cast<double*>(args.parts + (size_t)u * n_tiles + tile)[lane] = acc;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x < 11) {
-    double acc = 0.0;
-    for (int w = 0; w < 8; ++w) acc += s_red[threadIdx.x][w];
-    reinterpret_cast<double*>(args.parts + (size_t)u * gridDim.x + tile)[threadIdx.x] = acc;
-  }
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
-  }
-  if (last_block_arrive(args.counters + u, gridDim.x, &s_flag) && threadIdx.x == 0) {
-    const int stream = u / args.n_slots;
-    const long long base = args.first_slot >= 0
-        ? args.first_slot
-        : (long long)*reinterpret_cast<const int64_t*>(args.state + (size_t)stream * args.state_stride);
-    const long long slot = base + (u - stream * args.n_slots);
-    arches_telemetry tel;
-    finalize_unit(P, args.parts + (size_t)u * gridDim.x, gridDim.x,
-                  args.sigma2 ? args.sigma2 + u : nullptr, args.seeds ? args.seeds[stream] : 0ull,
-                  slot, 2, &tel, args.rng ? args.rng + 2 * u : nullptr);
-    args.tel[u] = tel;
-  }
-  (void)n_items;
+  tc_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// K3 -- per-unit finalisation for the tensor-core K2: reduce the tile partials
+// in tile order and derive both candidates (finalize_unit), one thread per unit.
+__global__ void k3_finalize(const PlanDev P, const K2Args args, int n_units) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int stream = u / args.n_slots;
+  const long long base = args.first_slot >= 0
+      ? args.first_slot
+      : (long long)*reinterpret_cast<const int64_t*>(args.state + (size_t)stream * args.state_stride);
+  const long long slot = base + (u - stream * args.n_slots);
+  arches_telemetry tel;
+  finalize_unit(P, args.parts + (size_t)u * P.n_tiles, P.n_tiles,
+                args.sigma2 ? args.sigma2 + u : nullptr, args.seeds ? args.seeds[stream] : 0ull,
+                slot, 2, &tel, args.rng ? args.rng + 2 * u : nullptr);
+  args.tel[u] = tel;
 }
