@@ -82,7 +82,7 @@ struct StreamState {
   int64_t mac_total, l4_total;
   int64_t last_delivery_ns;
   int32_t mode, ndi;
-  int32_t reserved1, reserved2;
+  int32_t prev_msg_mode, reserved2;   // oracle source: last_msg_mode one slot earlier
   int32_t n_pending, n_forced;
   int32_t since_decision, reserved3, reserved4, tripped;
   int32_t last_msg_mode, pad;

@@ -158,6 +158,7 @@ __global__ void k4_kpm_scan(const PlanDev P, const K4Args a) {
     const int64_t end_ns = (n + 1) * slot_ns;
     if (P.policy == ARCHES_POLICY_ORACLE) {
       const int want = (a.regime && a.regime[u]) ? 1 : 0;
+      st.prev_msg_mode = st.last_msg_mode;
       if (want != st.last_msg_mode) {
         PendingMsg m = {end_ns, want, ARCHES_TRIGGER_ORACLE};
         queue_insert(st.pending, st.n_pending, m);
@@ -216,6 +217,7 @@ __global__ void k4_state_init(const PlanDev P, void* state, int n_streams) {
   memset(&st, 0, sizeof(st));
   st.mode = 1;
   st.last_msg_mode = 1;
+  st.prev_msg_mode = 1;
   if (P.policy == ARCHES_POLICY_FIXED) {
     PendingMsg f = {0, P.fixed_mode, ARCHES_TRIGGER_FIXED};
     queue_insert(st.forced, st.n_forced, f);

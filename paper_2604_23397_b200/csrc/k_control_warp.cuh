@@ -122,12 +122,80 @@ __global__ void __launch_bounds__(32) k4_kpm_scan_warp(const PlanDev P, const K4
       const int g = (s0 + lane < a.n_slots && a.regime && a.regime[uu]) ? 1 : 0;
       good_mask = __ballot_sync(0xffffffffu, g);
     }
-    if (lane == 0) {
+    if (P.policy == ARCHES_POLICY_ORACLE && s_st.n_forced == 0) {
+      // Oracle source in closed form (every slot is independent given the
+      // regimes): after slot n the last message mode is L(n) = regime(n); a
+      // message is emitted iff regime(n) != L(n-1); it is applied at the next
+      // boundary (concurrent) or the one after (selected-only), so
+      // mode(n) = L(n-1) resp. L(n-2).  Identical to the sequential walk.
+      const int lim = min(32, a.n_slots - s0);
+      const bool act0 = lane < lim;
+      const int g = (good_mask >> lane) & 1;
+      int lm1 = __shfl_up_sync(0xffffffffu, g, 1);
+      int lm2 = __shfl_up_sync(0xffffffffu, g, 2);
+      if (lane == 0) lm1 = s_st.last_msg_mode;
+      if (lane == 0) lm2 = s_st.prev_msg_mode;
+      if (lane == 1) lm2 = s_st.last_msg_mode;
+      const bool sel = P.exec_mode == ARCHES_EXEC_SELECTED_ONLY;
+      const int mode = sel ? lm2 : lm1;
+      const int msg = (act0 && g != lm1) ? 1 : 0;
+      if (act0) s_mode[lane] = mode;
+      const unsigned int mm = __ballot_sync(0xffffffffu, msg);
+      const int cnt0 = a.msg_count ? a.msg_count[stream] : 0;
+      const int64_t n = s_st.next_slot + lane;
+      const int64_t end_ns = (n + 1) * slot_ns;
+      if (msg && a.msg_log) {
+        const int idx = cnt0 + __popc(mm & ((1u << lane) - 1u));
+        if (idx < a.msg_cap) {
+          arches_message m;
+          m.decided_at_ns = end_ns;
+          m.deliverable_at_ns = end_ns;
+          m.mode = g;
+          m.trigger = ARCHES_TRIGGER_ORACLE;
+          a.msg_log[(size_t)stream * a.msg_cap + idx] = m;
+        }
+      }
+      const int last = lim - 1;
+      const int g_last = __shfl_sync(0xffffffffu, g, last);
+      const int lm1_last = __shfl_sync(0xffffffffu, lm1, last);
+      const int mode_last = __shfl_sync(0xffffffffu, mode, last);
+      const int msg_l1 = __shfl_sync(0xffffffffu, msg, last);
+      const int msg_l2 = __shfl_sync(0xffffffffu, msg, last > 0 ? last - 1 : 0);
+      const int g_l2 = __shfl_sync(0xffffffffu, g, last > 0 ? last - 1 : 0);
+      if (lane == 0) {
+        StreamState& st = s_st;
+        const int64_t n_last = st.next_slot + last;
+        const int64_t cut = sel ? (n_last - 1) * slot_ns : n_last * slot_ns;  // begin_slot(n_last)
+        RegQueue pq;
+        pq.load(st.pending, st.n_pending);
+        RegQueue nq;
+        nq.load(st.pending, 0);  // empty, canonical zeros
+#pragma unroll
+        for (int i = 0; i < ARCHES_MAX_PENDING; ++i) nq.at[i] = 0, nq.mode[i] = 0, nq.trig[i] = 0;
+        for (int i = 0; i < ARCHES_MAX_PENDING; ++i) {
+          if (i >= pq.n) break;
+          if (pq.at[0] > cut) nq.insert(pq.at[0], pq.mode[0], pq.trig[0]);
+          pq.pop();
+        }
+        if (last > 0 && msg_l2 && n_last * slot_ns > cut)
+          nq.insert(n_last * slot_ns, g_l2, ARCHES_TRIGGER_ORACLE);
+        if (msg_l1 && (n_last + 1) * slot_ns > cut)
+          nq.insert((n_last + 1) * slot_ns, g_last, ARCHES_TRIGGER_ORACLE);
+        nq.store(st.pending, st.n_pending);
+        st.mode = mode_last;
+        st.prev_msg_mode = lm1_last;
+        st.last_msg_mode = g_last;
+        if (a.msg_count) a.msg_count[stream] = cnt0 + __popc(mm);
+        s_len = lim;
+        s_decide = 0;
+      }
+    } else if (lane == 0) {
       StreamState& st = s_st;
       RegQueue pq, fq;
       pq.load(st.pending, st.n_pending);
       fq.load(st.forced, st.n_forced);
-      int mode = st.mode, last_msg = st.last_msg_mode, since = st.since_decision;
+      int mode = st.mode, last_msg = st.last_msg_mode, prev_msg = st.prev_msg_mode;
+      int since = st.since_decision;
       int tripped = st.tripped;
       int64_t last_del = st.last_delivery_ns;
       int cnt = a.msg_count ? a.msg_count[stream] : 0;
@@ -150,6 +218,7 @@ __global__ void __launch_bounds__(32) k4_kpm_scan_warp(const PlanDev P, const K4
         const int64_t end_ns = t0 + slot_ns;
         if (P.policy == ARCHES_POLICY_ORACLE) {
           const int want = (good_mask >> j) & 1;
+          prev_msg = last_msg;
           if (want != last_msg) {
             pq.insert(end_ns, want, ARCHES_TRIGGER_ORACLE);
             last_msg = want;
@@ -174,6 +243,7 @@ __global__ void __launch_bounds__(32) k4_kpm_scan_warp(const PlanDev P, const K4
       fq.store(st.forced, st.n_forced);
       st.mode = mode;
       st.last_msg_mode = last_msg;
+      st.prev_msg_mode = prev_msg;
       st.since_decision = since;
       st.tripped = tripped;
       st.last_delivery_ns = last_del;
