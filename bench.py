@@ -321,7 +321,7 @@ def run_ours(a, rank, world, dist):
     if rank == 0:
         cpu = None
         if world == 1 and not a.no_cpu_baseline:
-            (rate, cores, sample), allres = cpu_reference_rate(a.n_prb, a.n_ant, 0, 2)
+            (rate, cores, sample), allres = cpu_reference_rate(a.n_prb, a.n_ant, 1, 2)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
                    "alternatives": {k: v[0] for k, v in allres.items()}}
         line = {
