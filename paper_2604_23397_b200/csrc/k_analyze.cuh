@@ -24,6 +24,7 @@ struct GridCombSrc {
   const float2* pil;  // [stream][M][D]
   int n_slots;
   static constexpr bool kComb = true;
+  static constexpr bool kGrid = true;
   __device__ __forceinline__ float2 load(const PlanDev& P, int u, int ad, int m) const {
     const int a = ad / P.D, d = ad - a * P.D;
     const float2 v = __ldg(&y[(((size_t)u * P.A + a) * P.T + P.dsym[d]) * P.N + 2 * m]);
@@ -37,6 +38,7 @@ struct GridCombSrc {
 struct LsCombSrc {
   const float2* ls;
   static constexpr bool kComb = true;
+  static constexpr bool kGrid = false;
   __device__ __forceinline__ float2 load(const PlanDev& P, int u, int ad, int m) const {
     return __ldg(&ls[((size_t)u * P.A * P.D + ad) * P.N + 2 * m]);
   }
@@ -45,6 +47,7 @@ struct LsCombSrc {
 struct LsFullSrc {
   const float2* ls;
   static constexpr bool kComb = false;
+  static constexpr bool kGrid = false;
   __device__ __forceinline__ float2 load(const PlanDev& P, int u, int ad, int k) const {
     return __ldg(&ls[((size_t)u * P.A * P.D + ad) * P.N + k]);
   }
@@ -113,7 +116,7 @@ __device__ inline void solve8_gram(const PlanDev& P, double s, double2* K /*[8][
 // In blocked-MMSE plans chunk == pilots per MMSE block, so a part's l < 8
 // partial bins are that block's bins (up to the block-origin phase).
 template <class Src>
-__global__ void __launch_bounds__(ARCHES_K1_THREADS)
+__global__ void __launch_bounds__(ARCHES_K1_THREADS, 3)
     k1_analyze(const PlanDev P, const Src src, const K1Out out, const int npts, const int chunk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_e[ARCHES_K1_THREADS / 32];
@@ -144,6 +147,52 @@ __global__ void __launch_bounds__(ARCHES_K1_THREADS)
   const int len = min(chunk, npts - base);
   // ---- LS of this part into smem (loads batched for memory-level parallelism)
   float e32 = 0.f;
+  if constexpr (Src::kGrid) {
+    if (chunk == ARCHES_K1_THREADS && AD <= 16) {
+      // one comb point per thread: pilots of its D symbols loaded once, the
+      // A*D received samples issued back to back
+      const int m = base + tid;
+      const bool okp = tid < len;
+      const float2* gsrc = reinterpret_cast<const GridCombSrc*>(&src)->y;
+      const float2* psrc = reinterpret_cast<const GridCombSrc*>(&src)->pil;
+      const int nsl = reinterpret_cast<const GridCombSrc*>(&src)->n_slots;
+      float2 pc[ARCHES_MAX_DMRS];
+      float pinv[ARCHES_MAX_DMRS];
+#pragma unroll
+      for (int d = 0; d < ARCHES_MAX_DMRS; ++d) {
+        pc[d] = (okp && d < P.D) ? __ldg(&psrc[((size_t)(u / nsl) * P.M + m) * P.D + d])
+                                 : make_float2(1.f, 0.f);
+        pinv[d] = 1.0f / (pc[d].x * pc[d].x + pc[d].y * pc[d].y);
+      }
+      float2 v[16];
+      const float2* yu = gsrc + (size_t)u * P.A * P.T * P.N + 2 * (size_t)m;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q < AD && okp) {
+          const int a = q / P.D, d = q - a * P.D;
+          v[q] = __ldg(&yu[((size_t)a * P.T + P.dsym[d]) * P.N]);
+        } else {
+          v[q] = make_float2(0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q < AD) {
+          const int d = q % P.D;
+          float2 pd = pc[0];
+          float pi = pinv[0];
+#pragma unroll
+          for (int dd = 1; dd < ARCHES_MAX_DMRS; ++dd)
+            if (d == dd) pd = pc[dd], pi = pinv[dd];
+          const float2 qv = cmulc(pd, v[q]);
+          const float2 h = make_float2(qv.x * pi, qv.y * pi);
+          hs[(size_t)q * chunk + tid] = h;
+          e32 = fmaf(h.x, h.x, fmaf(h.y, h.y, e32));
+        }
+      }
+      goto ls_done;
+    }
+  }
   {
     int ad = tid / chunk, jj = tid - ad * chunk;
     const int step_ad = ARCHES_K1_THREADS / chunk, step_j = ARCHES_K1_THREADS - step_ad * chunk;
@@ -172,6 +221,7 @@ __global__ void __launch_bounds__(ARCHES_K1_THREADS)
       }
     }
   }
+ls_done:
   __syncthreads();
   // ---- partial analysis bins: register tile RA x RL over a K-slice of points
   float2 acc[ARCHES_RA][ARCHES_RL];
