@@ -187,6 +187,32 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, u
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
 }
 
+// one symbol half (H) of the NR 0/5/10 pattern for one expert thread; SXX:
+// this thread also accumulates |x|^2 (expert-0 threads)
+template <int NA, int ND, int H, bool SXX>
+__device__ __forceinline__ void eq_std_half(const float2 (&h)[NA][ND], const float2* yrow,
+                                            const float2* xrow, float modd, float nv, float& sre,
+                                            float& sim, float& syy, float& sxx) {
+#pragma unroll
+  for (int tt = 0; tt < 7; ++tt) {
+    const int t = H * 7 + tt;
+    float wt[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) wt[d] = std_tw(t, d);
+    float2 yv[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) yv[a] = yrow[(size_t)(a * 14 + t) * ARCHES_TILE];
+    const float2 x = xrow[(size_t)t * ARCHES_TILE];
+    const bool dm = (t == 0 || t == 5 || t == 10);
+    const float m = dm ? modd : 1.f;
+    eq_re<NA, ND>(h, wt, yv, x, m, nv, sre, sim, syy);
+    if (SXX) {
+      if (dm) sxx = fmaf(m * x.x, x.x, fmaf(m * x.y, x.y, sxx));
+      else sxx = fmaf(x.x, x.x, fmaf(x.y, x.y, sxx));
+    }
+  }
+}
+
 // this thread's <= 2 B entries (output column pair r, tap l), fixed per thread
 struct BEntry {
   int r, l;
@@ -413,21 +439,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const float modd = (kk & 1) ? 1.f : 0.f;  // pilot REs: even k on DMRS symbols
       const float2* yrow = sYX + (size_t)buf * stage_elems + j;
       const float2* xrow = yrow + (size_t)P.A * T * ARCHES_TILE;
-      if (kStd) {
-#pragma unroll
-        for (int tt = 0; tt < 7; ++tt) {
-          const int t = half * 7 + tt;
-          float wt[ND];
-#pragma unroll
-          for (int d = 0; d < ND; ++d) wt[d] = half ? std_tw(7 + tt, d) : std_tw(tt, d);
-          float2 yv[NA];  // kStd plans have n_ant == NA exactly
-#pragma unroll
-          for (int a = 0; a < NA; ++a) yv[a] = yrow[(size_t)(a * 14 + t) * ARCHES_TILE];
-          const float2 x = xrow[(size_t)t * ARCHES_TILE];
-          const bool dm = half ? (7 + tt == 10) : (tt == 0 || tt == 5);
-          const float m = dm ? modd : 1.f;
-          eq_re<NA, ND>(h, wt, yv, x, m, nv, sre, sim, syy);
-          if (ex == 0) sxx = fmaf(m * x.x, x.x, fmaf(m * x.y, x.y, sxx));
+      if (kStd) {  // compile-time symbol half and expert: weights and pilot symbols fold
+        if (half == 0) {
+          if (ex == 0) eq_std_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
+          else         eq_std_half<NA, ND, 0, false>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
+        } else {
+          if (ex == 0) eq_std_half<NA, ND, 1, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
+          else         eq_std_half<NA, ND, 1, false>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
         }
       } else {
         const int t0 = half ? TH : 0, t1 = half ? T : TH;
