@@ -193,9 +193,11 @@ template <int NA, int ND, int H, bool SXX>
 __device__ __forceinline__ void eq_std_half(const float2 (&h)[NA][ND], const float2* yrow,
                                             const float2* xrow, float modd, float nv, float& sre,
                                             float& sim, float& syy, float& sxx) {
+  // balanced halves: 4 interpolated + 3 held symbols each
+  constexpr int kSym[2][7] = {{0, 1, 2, 3, 4, 5, 10}, {6, 7, 8, 9, 11, 12, 13}};
 #pragma unroll
   for (int tt = 0; tt < 7; ++tt) {
-    const int t = H * 7 + tt;
+    const int t = kSym[H][tt];
     float wt[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) wt[d] = std_tw(t, d);
@@ -281,8 +283,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 
   if (threadIdx.x == 0) {
-    mbar_init(&s_full[0], 1);
-    mbar_init(&s_full[1], 1);
+    mbar_init(&s_full[0], TC_THREADS / 32);  // one arrive.expect_tx per warp
+    mbar_init(&s_full[1], TC_THREADS / 32);
     mbar_init(&s_mma[0], 1);
     mbar_init(&s_mma[1], 1);
   }
@@ -297,15 +299,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = s_tmem;
   const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
 
-  auto issue_tma = [&](int item, int stage) {  // warp 0 (lanes split the rows)
+  auto issue_tma = [&](int item, int stage) {  // lane 0 of every warp: rows r = warp (mod 16)
     const int u = item / n_tiles, tile = item - u * n_tiles, k0 = tile * ARCHES_TILE;
     const uint32_t rowb = (uint32_t)min(ARCHES_TILE, P.N - k0) * sizeof(float2);
     const int rows = (P.A + 1) * T;
-    if (lane == 0) mbar_arrive_expect_tx(&s_full[stage], rowb * rows);
-    __syncwarp();
+    const int nw = TC_THREADS / 32;
+    const int mine = (rows - warp + nw - 1) / nw;  // rows of this warp
+    mbar_arrive_expect_tx(&s_full[stage], rowb * (uint32_t)mine);
     const uint64_t pol = l2_evict_first_policy();
     float2* dst = sYX + (size_t)stage * stage_elems;
-    for (int r = lane; r < rows; r += 32) {
+    for (int r = warp; r < rows; r += nw) {
       const float2* src = (r < P.A * T) ? args.y + ((size_t)u * P.A * T + r) * P.N + k0
                                         : args.tx + ((size_t)u * T + (r - P.A * T)) * P.N + k0;
       bulk_g2s(dst + (size_t)r * ARCHES_TILE, src, rowb, &s_full[stage], pol);
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int first = blockIdx.x;
   // ---- prologue: A operand (twiddle rows) -> TMEM, item 0 data + B(0) + MMA(0)
   if (first < n_items) {
-    if (warp == 0) issue_tma(first, 0);
+    if (lane == 0) issue_tma(first, 0);
     if (warp < 4) {
       const float4* arow = reinterpret_cast<const float4*>(P.tc_a) + (size_t)j * (KB * 4);
       for (int c = 0; c < KB; ++c) {
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int kk = k0 + j;
     const bool valid = kk < P.N;
     // ---- next item's data + coefficients in flight during this item's work
-    if (has_next && warp == 0) issue_tma(nxt, buf ^ 1);
+    if (has_next && lane == 0) issue_tma(nxt, buf ^ 1);
     float2 cv[2];
     if (has_next) {
       const int un = nxt / n_tiles;
