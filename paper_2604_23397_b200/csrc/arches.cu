@@ -1,5 +1,6 @@
 // C ABI of the ARCHES B200 hot path: plan construction, launch wrappers and
 // host helpers.  See include/arches.h for the contract of every entry point.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
@@ -492,6 +493,39 @@ static int experts_equalize_impl(const arches_plan* plan, int32_t n_streams, int
                                  void* h_mmse, void* h_ai, arches_telemetry* tel, void* ws,
                                  arches_stream_t stream, bool rng_from_k1);
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// [units][rows][N] complex64 viewed as fp32 [units][rows][2N]; box = one
+// 128-subcarrier tile of all rows of one unit
+static bool make_row_tmap(CUtensorMap* m, const void* base, int N, int rows, int units) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || (N & 1) || rows > 256 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * N, (cuuint64_t)rows, (cuuint64_t)units};
+  const cuuint64_t strides[2] = {(cuuint64_t)8 * N, (cuuint64_t)8 * N * rows};
+  const cuuint32_t box[3] = {2 * ARCHES_TILE, (cuuint32_t)rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cudaStream_t s) {
   const PlanDev& d = P->dev;
   const int n_items = n_units * d.n_tiles;
@@ -499,13 +533,19 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
   const size_t smem = P->k2_tc_smem;
   const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : 4;
   const bool std_pat = d.T == 14 && d.D == 3 && d.dsym[0] == 0 && d.dsym[1] == 5 && d.dsym[2] == 10;
+  CUtensorMap tm_y, tm_x;
+  memset(&tm_y, 0, sizeof(tm_y));
+  memset(&tm_x, 0, sizeof(tm_x));
+  const bool tmap = getenv("ARCHES_K2_NO_TMAP") == nullptr &&
+                    make_row_tmap(&tm_y, a.y, d.N, d.A * d.T, n_units) &&
+                    make_row_tmap(&tm_x, a.tx, d.N, d.T, n_units);
 #define K2TC_LAUNCH(NA_, ND_, STD_)                                                          \
   {                                                                                          \
-    auto kern = k2_tc<NA_, ND_, STD_>;                                                       \
-    CUDA_TRY(ensure_smem(kern, smem)); \
-    kern<<<grid, TC_THREADS, smem, s>>>(d, a, n_items);                                      \
+    auto kern = tmap ? k2_tc<NA_, ND_, STD_, true> : k2_tc<NA_, ND_, STD_, false>;           \
+    CUDA_TRY(ensure_smem(kern, smem));                                                       \
+    kern<<<grid, TC_THREADS, smem, s>>>(d, a, n_items, tm_y, tm_x);                          \
     LAUNCH_CHECK();                                                                          \
-    k3_finalize<<<(n_units + 127) / 128, 128, 0, s>>>(d, a, n_units);                        \
+    k3_finalize<<<(n_units + 127) / 128, 128, 0, s>>>(d, a, n_units, n_items, grid);         \
     LAUNCH_CHECK();                                                                          \
     return ARCHES_OK;                                                                        \
   }

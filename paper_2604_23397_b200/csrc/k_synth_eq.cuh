@@ -55,17 +55,11 @@ __device__ inline double lcid4_frac(const PlanDev& P, long long slot) {
   return fmin(fmax(f, 0.0), 1.0);
 }
 
-// last-CTA finalisation: reduce partials (tile order) and fill the telemetry
-__device__ inline void finalize_unit(const PlanDev& P, const TilePartial* parts, int n_tiles,
-                                     const double* sigma2, uint64_t seed, long long slot,
-                                     int n_experts, arches_telemetry* tel,
-                                     const double* rng = nullptr) {
-  double acc[11];
-  for (int i = 0; i < 11; ++i) acc[i] = 0.0;
-  for (int t = 0; t < n_tiles; ++t) {
-    const double* p = reinterpret_cast<const double*>(&parts[t]);
-    for (int i = 0; i < 11; ++i) acc[i] += p[i];
-  }
+// telemetry of one unit from its reduced sums acc[11] = {abs x2, pow x2, |x|^2,
+// Re x^H xhat x2, Im x2, |xhat|^2 x2}
+__device__ inline void finalize_acc(const PlanDev& P, const double (&acc)[11], const double* sigma2,
+                                    uint64_t seed, long long slot, int n_experts,
+                                    arches_telemetry* tel, const double* rng = nullptr) {
   const double cnt = (double)P.A * P.D * P.N;
   arches_telemetry out;
   out.sigma2_hat = sigma2 ? *sigma2 : 0.0;
@@ -81,6 +75,20 @@ __device__ inline void finalize_unit(const PlanDev& P, const TilePartial* parts,
                   out.crc[e], out.mac_rx[e], out.lcid4_rx[e]);
   }
   *tel = out;
+}
+
+// last-CTA finalisation: reduce partials (tile order) and fill the telemetry
+__device__ inline void finalize_unit(const PlanDev& P, const TilePartial* parts, int n_tiles,
+                                     const double* sigma2, uint64_t seed, long long slot,
+                                     int n_experts, arches_telemetry* tel,
+                                     const double* rng = nullptr) {
+  double acc[11];
+  for (int i = 0; i < 11; ++i) acc[i] = 0.0;
+  for (int t = 0; t < n_tiles; ++t) {
+    const double* p = reinterpret_cast<const double*>(&parts[t]);
+    for (int i = 0; i < 11; ++i) acc[i] += p[i];
+  }
+  finalize_acc(P, acc, sigma2, seed, slot, n_experts, tel, rng);
 }
 
 // block reduction of the per-thread partials into this tile's TilePartial

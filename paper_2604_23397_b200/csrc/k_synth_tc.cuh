@@ -17,6 +17,8 @@
 // Per-tile partial sums are reduced in a fixed order (fp32 per thread, fp64
 // across threads); the last tile of a unit finalises its telemetry.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 #include "k_synth_eq.cuh"
 
@@ -215,39 +217,31 @@ __device__ __forceinline__ void eq_std_half(const float2 (&h)[NA][ND], const flo
   }
 }
 
-// this thread's <= 2 B entries (output column pair r, tap l), fixed per thread
-struct BEntry {
-  int r, l;
-};
-
-template <int NA, int ND>
-__device__ __forceinline__ void load_b_entries(const PlanDev& P, const float2* coef_u, int tile,
-                                               const BEntry (&be)[2], float2 (&cv)[2]) {
-  constexpr int R = 2 * NA * ND;
-  const int L4 = 4 * P.tc_kb;
-  const int AD = P.A * ND;
-  const float2* cm = coef_u;
-  const float2* ca = cm + (size_t)AD * P.n_blocks * 8;
-  const float2* rot = P.tc_rot + (size_t)tile * (L4 + 8);
-  const int b = P.n_blocks == 1 ? 0 : min(tile * ARCHES_TILE / P.block, P.n_blocks - 1);
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int r = be[q].r, l = be[q].l;
-    float2 c = make_float2(0.f, 0.f);
-    if (r < NA * ND) {
-      if (r < AD && l < P.trunc) c = cmul(__ldg(&ca[r * P.trunc + l]), __ldg(&rot[l]));
-    } else if (r < R) {
-      const int ad = r - NA * ND;
-      if (ad < AD && l < 8)
-        c = cmul(__ldg(&cm[((size_t)ad * P.n_blocks + b) * 8 + l]), __ldg(&rot[L4 + l]));
-    }
-    cv[q] = c;
-  }
+// 3-D tensor TMA: box {256 floats, rows, 1} of a [units][rows][2N floats] array
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
+      "l"(policy)
+      : "memory");
 }
 
-template <int NA, int ND, bool kStd>
+// Work split: CTA b owns the contiguous item range [b*n/G, (b+1)*n/G), so a
+// CTA walks the tiles of one unit in order and its threads keep their
+// telemetry sums in registers across them; a unit's sums are flushed once per
+// (CTA, unit) segment, at the segment's first tile.  K3 adds the segments.
+__host__ __device__ inline bool k2_segment_start(int item, int n_tiles, int n_items, int G) {
+  if (item % n_tiles == 0) return true;
+  const long long b = ((long long)item * G + n_items - 1) / n_items;  // ceil
+  return b < G && (b * n_items) / G == item;
+}
+
+template <int NA, int ND, bool kStd, bool kTmap>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    k2_tc(const PlanDev P, const K2Args args, const int n_items) {
+    k2_tc(const PlanDev P, const K2Args args, const int n_items,
+          const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ CUtensorMap tm_x) {
   constexpr int R = 2 * NA * ND;                    // complex outputs: AI then MMSE
   constexpr int NCOL = ((2 * R + 15) / 16) * 16;    // MMA N (real columns)
   constexpr int NG = NCOL / 8;
@@ -268,23 +262,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int AD = P.A * ND;
   const int n_tiles = P.n_tiles;
   const int G = gridDim.x;
+  const int lo = (int)((long long)blockIdx.x * n_items / G);
+  const int hi = (int)((long long)(blockIdx.x + 1) * n_items / G);
   const uint32_t b_bytes = (uint32_t)KB * NG * 256;
   const size_t stage_elems = (size_t)(P.A + 1) * T * ARCHES_TILE;
+  const size_t coef_stride = coef_floats2(P);
   float2* sYX = reinterpret_cast<float2*>(sm);                               // [2][stage]
   unsigned char* sB = sm + 2 * stage_elems * sizeof(float2);                 // [2][hi | lo]
   const int n_all = (NCOL / 2) * L4;                                         // B entries
   const uint32_t ACC0 = 128;                                                 // TMEM columns
-  BEntry be[2];
+  // this thread's <= 2 B entries (output column pair r, tap l): source offsets
+  // inside a unit's coefficients, rotation index, shared-memory offsets
+  int boff[2], roff[2];
+  bool bmm[2];
+  uint32_t o0[2], o1[2];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int e = threadIdx.x + q * TC_THREADS;
-    be[q].r = e < n_all ? e / L4 : (1 << 20);  // out of range -> zero, skipped
-    be[q].l = e < n_all ? e - be[q].r * L4 : 0;
+    boff[q] = -1; roff[q] = 0; bmm[q] = false; o0[q] = o1[q] = 0;
+    if (e < n_all) {
+      const int r = e / L4, l = e - r * L4;
+      o0[q] = kmaj_off(2 * r, 2 * l, NG);
+      o1[q] = kmaj_off(2 * r + 1, 2 * l, NG);
+      if (r < NA * ND) {
+        if (r < AD && l < P.trunc) { boff[q] = AD * P.n_blocks * 8 + r * P.trunc + l; roff[q] = l; }
+      } else if (r < R) {
+        const int ad = r - NA * ND;
+        if (ad < AD && l < 8) { boff[q] = ad * P.n_blocks * 8 + l; roff[q] = L4 + l; bmm[q] = true; }
+      }
+    }
   }
 
   if (threadIdx.x == 0) {
-    mbar_init(&s_full[0], TC_THREADS / 32);  // one arrive.expect_tx per warp
-    mbar_init(&s_full[1], TC_THREADS / 32);
+    const uint32_t arrivals = kTmap ? 1u : (uint32_t)(TC_THREADS / 32);
+    mbar_init(&s_full[0], arrivals);
+    mbar_init(&s_full[1], arrivals);
     mbar_init(&s_mma[0], 1);
     mbar_init(&s_mma[1], 1);
   }
@@ -299,36 +311,52 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = s_tmem;
   const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
 
-  auto issue_tma = [&](int item, int stage) {  // lane 0 of every warp: rows r = warp (mod 16)
-    const int u = item / n_tiles, tile = item - u * n_tiles, k0 = tile * ARCHES_TILE;
-    const uint32_t rowb = (uint32_t)min(ARCHES_TILE, P.N - k0) * sizeof(float2);
-    const int rows = (P.A + 1) * T;
-    const int nw = TC_THREADS / 32;
-    const int mine = (rows - warp + nw - 1) / nw;  // rows of this warp
-    mbar_arrive_expect_tx(&s_full[stage], rowb * (uint32_t)mine);
+  auto issue_tma = [&](int u, int tile, int stage) {
     const uint64_t pol = l2_evict_first_policy();
     float2* dst = sYX + (size_t)stage * stage_elems;
-    for (int r = warp; r < rows; r += nw) {
-      const float2* src = (r < P.A * T) ? args.y + ((size_t)u * P.A * T + r) * P.N + k0
-                                        : args.tx + ((size_t)u * T + (r - P.A * T)) * P.N + k0;
-      bulk_g2s(dst + (size_t)r * ARCHES_TILE, src, rowb, &s_full[stage], pol);
+    if constexpr (kTmap) {  // thread 0: two tensor copies (y rows, tx rows)
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&s_full[stage], (uint32_t)(stage_elems * sizeof(float2)));
+        tma_load_3d(dst, &tm_y, tile * 2 * ARCHES_TILE, 0, u, &s_full[stage], pol);
+        tma_load_3d(dst + (size_t)P.A * T * ARCHES_TILE, &tm_x, tile * 2 * ARCHES_TILE, 0, u,
+                    &s_full[stage], pol);
+      }
+    } else if (lane == 0) {  // lane 0 of every warp: rows r = warp (mod 16)
+      const int k0 = tile * ARCHES_TILE;
+      const uint32_t rowb = (uint32_t)min(ARCHES_TILE, P.N - k0) * sizeof(float2);
+      const int rows = (P.A + 1) * T;
+      const int nw = TC_THREADS / 32;
+      const int mine = (rows - warp + nw - 1) / nw;
+      mbar_arrive_expect_tx(&s_full[stage], rowb * (uint32_t)mine);
+      for (int r = warp; r < rows; r += nw) {
+        const float2* src = (r < P.A * T) ? args.y + ((size_t)u * P.A * T + r) * P.N + k0
+                                          : args.tx + ((size_t)u * T + (r - P.A * T)) * P.N + k0;
+        bulk_g2s(dst + (size_t)r * ARCHES_TILE, src, rowb, &s_full[stage], pol);
+      }
     }
   };
-  auto write_b = [&](int buf, const float2* cv) {  // this thread's <= 2 entries
+  auto load_b = [&](int u, int tile, float2 (&cv)[2]) {  // coefficients rotated to the tile
+    const float2* cu = args.coef + (size_t)u * coef_stride;
+    const float2* rot = P.tc_rot + (size_t)tile * (L4 + 8);
+    const int bo = P.n_blocks == 1 ? 0 : min(tile * ARCHES_TILE / P.block, P.n_blocks - 1) * 8;
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      cv[q] = boff[q] >= 0 ? cmul(__ldg(&cu[boff[q] + (bmm[q] ? bo : 0)]), __ldg(&rot[roff[q]]))
+                           : make_float2(0.f, 0.f);
+  };
+  auto write_b = [&](int buf, const float2 (&cv)[2]) {
     unsigned char* bhi = sB + (size_t)buf * 2 * b_bytes;
     unsigned char* blo = bhi + b_bytes;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      if (be[q].r >= (1 << 20)) break;
-      const int r = be[q].r, l = be[q].l;
+      if (q * TC_THREADS + (int)threadIdx.x >= n_all) break;
       const float2 c = cv[q];
       const float rh = tf32_rna(c.x), rl = tf32_rna(c.x - rh);
       const float ih = tf32_rna(c.y), il = tf32_rna(c.y - ih);
-      const uint32_t o0 = kmaj_off(2 * r, 2 * l, NG), o1 = kmaj_off(2 * r + 1, 2 * l, NG);
-      *reinterpret_cast<float2*>(bhi + o0) = make_float2(rh, -ih);
-      *reinterpret_cast<float2*>(bhi + o1) = make_float2(ih, rh);
-      *reinterpret_cast<float2*>(blo + o0) = make_float2(rl, -il);
-      *reinterpret_cast<float2*>(blo + o1) = make_float2(il, rl);
+      *reinterpret_cast<float2*>(bhi + o0[q]) = make_float2(rh, -ih);
+      *reinterpret_cast<float2*>(bhi + o1[q]) = make_float2(ih, rh);
+      *reinterpret_cast<float2*>(blo + o0[q]) = make_float2(rl, -il);
+      *reinterpret_cast<float2*>(blo + o1[q]) = make_float2(il, rl);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   };
@@ -349,10 +377,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     umma_commit(&s_mma[buf]);
   };
 
-  const int first = blockIdx.x;
+  int u = lo / n_tiles, tile = lo - u * n_tiles;
   // ---- prologue: A operand (twiddle rows) -> TMEM, item 0 data + B(0) + MMA(0)
-  if (first < n_items) {
-    if (lane == 0) issue_tma(first, 0);
+  if (lo < hi) {
+    issue_tma(u, tile, 0);
     if (warp < 4) {
       const float4* arow = reinterpret_cast<const float4*>(P.tc_a) + (size_t)j * (KB * 4);
       for (int c = 0; c < KB; ++c) {
@@ -378,32 +406,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     float2 cv[2];
-    const int u0 = first / n_tiles;
-    load_b_entries<NA, ND>(P, args.coef + (size_t)u0 * coef_floats2(P), first - u0 * n_tiles, be, cv);
+    load_b(u, tile, cv);
     write_b(0, cv);
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) issue_mma(0);
   }
 
-  for (int i = 0;; ++i) {
-    const int item = first + i * G;
-    if (item >= n_items) break;
+  // per-thread telemetry sums, kept across the tiles of one unit
+  float sa = 0.f, sp = 0.f, sre = 0.f, sim = 0.f, syy = 0.f, sxx = 0.f;
+  int seg_t0 = tile;  // first tile of the current (CTA, unit) segment
+  float nv = lo < hi ? (float)__ldg(&args.nv[u]) : 0.f;
+  for (int item = lo, i = 0; item < hi; ++item, ++i) {
     const int buf = i & 1, ph = (i >> 1) & 1;
-    const int nxt = item + G;
-    const bool has_next = nxt < n_items;
-    const int u = item / n_tiles, tile = item - u * n_tiles;
+    const bool has_next = item + 1 < hi;
+    const bool last_tile = tile + 1 == n_tiles;
+    const int un = last_tile ? u + 1 : u, tn = last_tile ? 0 : tile + 1;
+    const bool flush = last_tile || !has_next;
     const int k0 = tile * ARCHES_TILE;
     const int kk = k0 + j;
     const bool valid = kk < P.N;
     // ---- next item's data + coefficients in flight during this item's work
-    if (has_next && lane == 0) issue_tma(nxt, buf ^ 1);
     float2 cv[2];
     if (has_next) {
-      const int un = nxt / n_tiles;
-      load_b_entries<NA, ND>(P, args.coef + (size_t)un * coef_floats2(P), nxt - un * n_tiles, be, cv);
+      issue_tma(un, tn, buf ^ 1);
+      load_b(un, tn, cv);
     }
-    const float nv = (float)__ldg(&args.nv[u]);
     // ---- this expert's synthesised taps
     mbar_wait(&s_mma[buf], ph);
     tc_fence_after();
@@ -416,7 +444,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
       for (int d = 0; d < ND; ++d)
         h[a][d] = make_float2(vals[2 * (a * ND + d)], vals[2 * (a * ND + d) + 1]);
-    float sa = 0.f, sp = 0.f, sre = 0.f, sim = 0.f, syy = 0.f, sxx = 0.f;
     float2* hout = ex ? args.h_mmse : args.h_ai;
     if (valid && half == 0 && hout) {  // half 0 stores the expert output ...
       float2* o = hout + (size_t)u * AD * P.N + kk;
@@ -432,7 +459,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int d = 0; d < ND; ++d) {
           const float p2 = fmaf(h[a][d].x, h[a][d].x, h[a][d].y * h[a][d].y);
-          sa += sqrtf(p2);
+          float r;
+          asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p2));
+          sa += r;
           sp += p2;
         }
     }
@@ -467,9 +496,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
-    // ---- per-warp partials -> s_red[buf] (column = half*4 + quarter order)
-    {
-      const int col = half * 4 + (q4 ^ 0);
+    // ---- end of a (CTA, unit) segment: per-warp partials -> s_red[buf]
+    if (flush) {
+      const int col = half * 4 + q4;
       const double r2 = warp_sum((double)sre), r3 = warp_sum((double)sim);
       const double r4 = warp_sum((double)syy);
       double r0 = 0.0, r1 = 0.0, r5 = 0.0;
@@ -488,14 +517,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         s_red[buf][7 + ex][col] = r3;
         s_red[buf][9 + ex][col] = r4;
       }
+      sa = sp = sre = sim = syy = sxx = 0.f;
     }
     // ---- B(i+1) -> shared memory, one barrier, MMA(i+1)
     if (has_next) write_b(buf ^ 1, cv);
     tc_fence_before();
     __syncthreads();
     if (has_next && threadIdx.x == 0) issue_mma(buf ^ 1);
-    // ---- tile partial (fixed order); per-unit finalisation runs in K3
-    if (warp == 1 && lane < 11) {
+    // ---- segment partial (fixed order); per-unit finalisation runs in K3
+    if (flush && warp == 1 && lane < 11) {
       double acc;
       if (lane < 4) {  // abs / pow: half 1 only
         acc = ((s_red[buf][lane][0] + s_red[buf][lane][1]) + s_red[buf][lane][2]) + s_red[buf][lane][3];
@@ -503,8 +533,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         acc = 0.0;
         for (int w = 0; w < 8; ++w) acc += s_red[buf][lane][w];
       }
-      reinterpret_cast<double*>(args.parts + (size_t)u * n_tiles + tile)[lane] = acc;
+      reinterpret_cast<double*>(args.parts + (size_t)u * n_tiles + seg_t0)[lane] = acc;
     }
+    if (last_tile) {
+      seg_t0 = 0;
+      if (has_next) nv = (float)__ldg(&args.nv[un]);
+    }
+    u = un;
+    tile = tn;
   }
   tc_fence_before();
   __syncthreads();
@@ -515,7 +551,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // K3 -- per-unit finalisation for the tensor-core K2: reduce the tile partials
 // in tile order and derive both candidates (finalize_unit), one thread per unit.
-__global__ void k3_finalize(const PlanDev P, const K2Args args, int n_units) {
+__global__ void k3_finalize(const PlanDev P, const K2Args args, int n_units, int n_items, int G) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n_units) return;
   const int stream = u / args.n_slots;
@@ -523,9 +559,15 @@ __global__ void k3_finalize(const PlanDev P, const K2Args args, int n_units) {
       ? args.first_slot
       : (long long)*reinterpret_cast<const int64_t*>(args.state + (size_t)stream * args.state_stride);
   const long long slot = base + (u - stream * args.n_slots);
+  double acc[11];
+  for (int i = 0; i < 11; ++i) acc[i] = 0.0;
+  for (int t = 0; t < P.n_tiles; ++t) {  // segment partials in tile order
+    if (!k2_segment_start(u * P.n_tiles + t, P.n_tiles, n_items, G)) continue;
+    const double* p = reinterpret_cast<const double*>(args.parts + (size_t)u * P.n_tiles + t);
+    for (int i = 0; i < 11; ++i) acc[i] += p[i];
+  }
   arches_telemetry tel;
-  finalize_unit(P, args.parts + (size_t)u * P.n_tiles, P.n_tiles,
-                args.sigma2 ? args.sigma2 + u : nullptr, args.seeds ? args.seeds[stream] : 0ull,
-                slot, 2, &tel, args.rng ? args.rng + 2 * u : nullptr);
+  finalize_acc(P, acc, args.sigma2 ? args.sigma2 + u : nullptr, args.seeds ? args.seeds[stream] : 0ull,
+               slot, 2, &tel, args.rng ? args.rng + 2 * u : nullptr);
   args.tel[u] = tel;
 }
