@@ -545,7 +545,7 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
     CUDA_TRY(ensure_smem(kern, smem));                                                       \
     kern<<<grid, TC_THREADS, smem, s>>>(d, a, n_items, tm_y, tm_x);                          \
     LAUNCH_CHECK();                                                                          \
-    k3_finalize<<<(n_units + 127) / 128, 128, 0, s>>>(d, a, n_units, n_items, grid);         \
+    k3_finalize<<<(n_units * 32 + K3_THREADS - 1) / K3_THREADS, K3_THREADS, 0, s>>>(d, a, n_units, n_items, grid); \
     LAUNCH_CHECK();                                                                          \
     return ARCHES_OK;                                                                        \
   }
@@ -583,7 +583,8 @@ static int experts_equalize_impl(const arches_plan* plan, int32_t n_streams, int
   const int n_units = n_streams * n_slots;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const WsLayout w = ws_layout(plan, n_units);
-  CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.counters), 0, n_units * sizeof(unsigned int), s));
+  if (!plan->k2_tc_smem)  // the FFMA form's last-CTA counters (the tensor-core form uses K3)
+    CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.counters), 0, n_units * sizeof(unsigned int), s));
   K2Args a;
   memset(&a, 0, sizeof(a));
   a.y = reinterpret_cast<const float2*>(y);

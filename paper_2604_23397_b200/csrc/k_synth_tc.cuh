@@ -549,25 +549,64 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-// K3 -- per-unit finalisation for the tensor-core K2: reduce the tile partials
-// in tile order and derive both candidates (finalize_unit), one thread per unit.
-__global__ void k3_finalize(const PlanDev P, const K2Args args, int n_units, int n_items, int G) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= n_units) return;
-  const int stream = u / args.n_slots;
-  const long long base = args.first_slot >= 0
-      ? args.first_slot
-      : (long long)*reinterpret_cast<const int64_t*>(args.state + (size_t)stream * args.state_stride);
-  const long long slot = base + (u - stream * args.n_slots);
+// K3 -- per-unit finalisation for the tensor-core K2, one warp per unit: lanes
+// fetch the (CTA, unit) segment partials in parallel, the sum runs in tile
+// order (segments only -- the other tiles hold no partial), then lanes 0 / 1
+// derive the AI / MMSE candidate (link adaptation, TB, CRC, MAC split).
+#define K3_THREADS 128
+__global__ void __launch_bounds__(K3_THREADS) k3_finalize(const PlanDev P, const K2Args args,
+                                                          int n_units, int n_items, int G) {
+  const int u = (int)((blockIdx.x * (unsigned)K3_THREADS + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (u >= n_units) return;  // warp-uniform
   double acc[11];
+#pragma unroll
   for (int i = 0; i < 11; ++i) acc[i] = 0.0;
-  for (int t = 0; t < P.n_tiles; ++t) {  // segment partials in tile order
-    if (!k2_segment_start(u * P.n_tiles + t, P.n_tiles, n_items, G)) continue;
+  for (int t0 = 0; t0 < P.n_tiles; t0 += 32) {
+    const int t = t0 + lane;
+    const bool seg = t < P.n_tiles && k2_segment_start(u * P.n_tiles + t, P.n_tiles, n_items, G);
+    double v[11];
     const double* p = reinterpret_cast<const double*>(args.parts + (size_t)u * P.n_tiles + t);
-    for (int i = 0; i < 11; ++i) acc[i] += p[i];
+#pragma unroll
+    for (int i = 0; i < 11; ++i) v[i] = seg ? p[i] : 0.0;
+    unsigned int m = __ballot_sync(0xffffffffu, seg);
+    while (m) {  // ascending tile order, identical on every lane
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+#pragma unroll
+      for (int i = 0; i < 11; ++i) acc[i] += __shfl_sync(0xffffffffu, v[i], src);
+    }
   }
-  arches_telemetry tel;
-  finalize_acc(P, acc, args.sigma2 ? args.sigma2 + u : nullptr, args.seeds ? args.seeds[stream] : 0ull,
-               slot, 2, &tel, args.rng ? args.rng + 2 * u : nullptr);
-  args.tel[u] = tel;
+  if (lane >= 2) return;
+  const int e = lane;  // 0 = AI, 1 = MMSE
+  const int stream = u / args.n_slots;
+  const double* rng = args.rng ? args.rng + 2 * u : nullptr;
+  double u_crc, frac;
+  if (rng) {
+    u_crc = rng[0];
+    frac = rng[1];
+  } else {
+    const long long base = args.first_slot >= 0
+        ? args.first_slot
+        : (long long)*reinterpret_cast<const int64_t*>(args.state + (size_t)stream * args.state_stride);
+    const long long slot = base + (u - stream * args.n_slots);
+    u_crc = arches_rng::stream_first_uniform(args.seeds ? args.seeds[stream] : 0ull, P.crc_key,
+                                             (uint64_t)slot);
+    frac = lcid4_frac(P, slot);
+  }
+  const double cnt = (double)P.A * P.D * P.N;
+  arches_telemetry* tel = args.tel + u;
+  if (e == 0) tel->sigma2_hat = args.sigma2 ? args.sigma2[u] : 0.0;
+  tel->abs_mean[e] = acc[0 + e] / cnt;
+  tel->rsrp[e] = acc[2 + e] / cnt;
+  const double sinr = sinr_from_sums(acc[4], acc[5 + e], acc[7 + e], acc[9 + e], P.sinr_cap_db);
+  tel->sinr_db[e] = sinr;
+  int mcs, tb, ncb, crc, mac_rx, l4_rx;
+  kpm_candidate(P, sinr, u_crc, frac, mcs, tb, ncb, crc, mac_rx, l4_rx);
+  tel->mcs[e] = mcs;
+  tel->tb_bytes[e] = tb;
+  tel->num_cb[e] = ncb;
+  tel->crc[e] = crc;
+  tel->mac_rx[e] = mac_rx;
+  tel->lcid4_rx[e] = l4_rx;
 }
