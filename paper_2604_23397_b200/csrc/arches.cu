@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "k_analyze.cuh"
+#include "k_analyze_tc.cuh"
 #include "k_control.cuh"
 #include "k_control_warp.cuh"
 #include "k_synth_eq.cuh"
@@ -57,6 +58,10 @@ struct arches_plan {
   int k1_chunk;        // K1 points per CTA (comb analysis)
   int k1_parts;        // K1 CTAs per unit (comb analysis)
   size_t k1_smem;
+  int k1t_nb;          // tensor-core K1: MMA N (0 = not applicable)
+  int k1t_nchunks;     // 16-subcarrier chunks per row
+  float* k1t_wimg;     // twiddle operand [hi|lo][kg][nb][4] (chunk-invariant)
+  float2* k1t_rot;     // chunk phases [chunk][L]
   int k1_full_chunk;   // N-point (denoiser compat) variant
   int k1_full_parts;
   size_t k1_full_smem;
@@ -84,8 +89,15 @@ static cudaError_t ensure_smem(K kern, size_t smem) {
 
 // ------------------------------------------------------------ workspace
 struct WsLayout {
-  size_t coef, parts, counters, k1parts, k1counters, sigma2, rng, total;
+  size_t coef, parts, counters, k1parts, k1counters, sigma2, rng, k1t_d, k1t_e, total;
 };
+
+// tensor-core K1 work split: 128-row tiles x DMRS symbols x subcarrier parts,
+// parts chosen so the items fill (at most) one wave of SMs
+struct K1TGeom {
+  int n_g, parts, cpp, n_items;
+};
+static K1TGeom k1t_geom(const arches_plan* P, int n_units);
 
 static WsLayout ws_layout(const arches_plan* P, int n_units) {
   const PlanDev& d = P->dev;
@@ -108,6 +120,14 @@ static WsLayout ws_layout(const arches_plan* P, int n_units) {
   off += align256((size_t)n_units * sizeof(double));
   w.rng = off;
   off += align256((size_t)n_units * 2 * sizeof(double));
+  w.k1t_d = w.k1t_e = off;
+  if (P->k1t_nb) {
+    const K1TGeom kg = k1t_geom(P, n_units);
+    w.k1t_d = off;
+    off += align256((size_t)kg.n_items * 128 * 2 * d.L * sizeof(double));
+    w.k1t_e = off;
+    off += align256((size_t)kg.n_items * 128 * sizeof(double));
+  }
   w.total = off;
   return w;
 }
@@ -371,6 +391,65 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
     return stage * sizeof(float2) + (size_t)AD * d.L * sizeof(double2) + 64 * sizeof(double2);
   };
   P->k1_smem = k1_smem(chunk);
+  {
+    // tensor-core K1: one MMSE block (closed-form taps), <= 4 DMRS symbols, 2L <= 128
+    P->k1t_nb = 0;
+    P->k1t_wimg = nullptr;
+    P->k1t_nchunks = (N + K1T_CSC - 1) / K1T_CSC;
+    const int nb = ((2 * d.L + 15) / 16) * 16;
+    if (d.diag && d.D <= 4 && d.L == 20 && P->k1t_nchunks <= K1T_MAX_CHUNKS &&
+        !getenv("ARCHES_DISABLE_K1T")) {  // k1_tc<48, 40>
+      // chunk-invariant operand W[p][l] = e^{2 pi i l p / M} (p < 16 comb points),
+      // real-embedded: kappa = 2p + (0: Re h, 1: Im h), row n = 2l + (0: Re, 1: Im);
+      // [n][32 floats] in the SWIZZLE_128B layout, tf32 hi then lo
+      const size_t half = (size_t)nb * 32;  // floats of one of hi | lo
+      std::vector<float> img(2 * half, 0.f);
+      auto tf32 = [](float x) {
+        uint32_t b;
+        memcpy(&b, &x, 4);
+        b = (b + 0x1000u) & 0xFFFFE000u;
+        float r;
+        memcpy(&r, &b, 4);
+        return r;
+      };
+      for (int pp = 0; pp < K1T_CP; ++pp)
+        for (int n = 0; n < 2 * d.L; ++n) {
+          const int l = n >> 1;
+          const long long idx = ((long long)l * pp) % M;
+          const double ang = 2.0 * M_PI * (double)idx / (double)M;
+          const float wr = (float)cos(ang), wi = (float)sin(ang);
+          const float bv[2] = {(n & 1) ? wi : wr, (n & 1) ? wr : -wi};
+          for (int cc = 0; cc < 2; ++cc) {
+            const int kap = 2 * pp + cc, grp = kap >> 2;
+            const float hi = tf32(bv[cc]), lo = tf32(bv[cc] - hi);
+            const size_t o = (size_t)n * 32 + (size_t)((grp ^ (n & 7)) * 4) + (kap & 3);
+            img[o] = hi;
+            img[half + o] = lo;
+          }
+        }
+      // chunk phases e^{2 pi i l 16c / M}
+      std::vector<float2> rot((size_t)P->k1t_nchunks * d.L);
+      for (int c = 0; c < P->k1t_nchunks; ++c)
+        for (int l = 0; l < d.L; ++l) {
+          const long long idx = ((long long)l * K1T_CP * c) % M;
+          const double ang = 2.0 * M_PI * (double)idx / (double)M;
+          rot[(size_t)c * d.L + l] = make_float2((float)cos(ang), (float)sin(ang));
+        }
+      const size_t rot_off = (img.size() * sizeof(float) + 255) & ~(size_t)255;
+      unsigned char* dimg = nullptr;
+      const size_t bytes = rot_off + rot.size() * sizeof(float2);
+      if (cudaMalloc(&dimg, bytes) == cudaSuccess &&
+          cudaMemcpy(dimg, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice) == cudaSuccess &&
+          cudaMemcpy(dimg + rot_off, rot.data(), rot.size() * sizeof(float2), cudaMemcpyHostToDevice) ==
+              cudaSuccess) {
+        P->k1t_wimg = reinterpret_cast<float*>(dimg);
+        P->k1t_rot = reinterpret_cast<float2*>(dimg + rot_off);
+        P->k1t_nb = nb;
+      } else if (dimg) {
+        cudaFree(dimg);
+      }
+    }
+  }
   P->k1_full_chunk = std::max(32, std::min(256, (8192 / AD) / 32 * 32));
   P->k1_full_parts = (N + P->k1_full_chunk - 1) / P->k1_full_chunk;
   P->k1_full_smem = k1_smem(P->k1_full_chunk);
@@ -401,6 +480,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
 extern "C" int arches_plan_destroy(arches_plan* plan) {
   if (!plan) return ARCHES_OK;
   if (plan->dev_tables) cudaFree(plan->dev_tables);
+  if (plan->k1t_wimg) cudaFree(plan->k1t_wimg);
   delete plan;
   return ARCHES_OK;
 }
@@ -437,6 +517,97 @@ static int launch_k1(const arches_plan* P, int n_units, const Src& src, const K1
   return ARCHES_OK;
 }
 
+static K1TGeom k1t_geom(const arches_plan* P, int n_units) {
+  const PlanDev& d = P->dev;
+  K1TGeom g;
+  g.n_g = (n_units * d.A + 127) / 128;
+  const int base = g.n_g * d.D;
+  int parts = std::max(1, d.num_sms / std::max(1, base));
+  parts = std::min(parts, P->k1t_nchunks);
+  g.cpp = (P->k1t_nchunks + parts - 1) / parts;
+  g.parts = (P->k1t_nchunks + g.cpp - 1) / g.cpp;
+  g.n_items = base * g.parts;
+  return g;
+}
+
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled();
+
+// DMRS symbol d of every (unit, antenna) row as a 2-D fp32 view {2N floats,
+// rows}; box {32 floats, 128 rows} lands 128 rows x 16 subcarriers in the
+// UMMA K-major SWIZZLE_128B layout
+static bool make_k1t_tmap(CUtensorMap* m, const float2* y, const PlanDev& d, int dsym, int rows) {
+  EncodeTiledFn enc = encode_tiled();
+  const float2* base = y + (size_t)dsym * d.N;
+  if (!enc || (d.N & 1) || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)2 * d.N, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)8 * d.T * d.N};
+  const cuuint32_t box[2] = {32, 128};  // 128 B (the swizzle span) x 128 rows
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int launch_k1t(const arches_plan* P, int n_units, const GridCombSrc& src, const K1Out& o,
+                      const WsLayout& w, void* ws, cudaStream_t s) {
+  const PlanDev& d = P->dev;
+  const K1TGeom kg = k1t_geom(P, n_units);
+  K1TArgs a;
+  a.pil = src.pil;
+  a.wimg = P->k1t_wimg;
+  a.rot = P->k1t_rot;
+  a.dpart = ws_at<double>(ws, w.k1t_d);
+  a.epart = ws_at<double>(ws, w.k1t_e);
+  a.n_slots = src.n_slots;
+  a.n_rows = n_units * d.A;
+  a.n_g = kg.n_g;
+  a.parts = kg.parts;
+  a.cpp = kg.cpp;
+  a.n_chunks = P->k1t_nchunks;
+  a.nb = P->k1t_nb;
+  CUtensorMap tm[4];
+  memset(tm, 0, sizeof(tm));
+  for (int dd = 0; dd < d.D; ++dd)
+    if (!make_k1t_tmap(&tm[dd], src.y, d, d.dsym[dd], a.n_rows))
+      return set_err(ARCHES_E_CUDA, "K1: tensor map encode failed");
+  const int grid = std::min(kg.n_items, d.num_sms);
+  const size_t smem = k1t_smem_bytes(a.nb);
+  a.dbg = nullptr;
+  static long long* dbg_buf = nullptr;
+  const bool dbg = getenv("ARCHES_K1T_DBG") != nullptr;  // profiling aid: wait cycles per role
+  if (dbg) {
+    if (!dbg_buf) cudaMalloc(&dbg_buf, 1024 * 8 * sizeof(long long));
+    cudaMemsetAsync(dbg_buf, 0, 1024 * 8 * sizeof(long long), s);
+    a.dbg = dbg_buf;
+  }
+  struct DbgPrint {
+    bool on; long long* buf; int g; cudaStream_t s;
+    ~DbgPrint() {
+      if (!on) return;
+      std::vector<long long> h(g * 8);
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h.data(), buf, g * 8 * sizeof(long long), cudaMemcpyDeviceToHost);
+      double acc[8] = {0};
+      for (int b = 0; b < g; ++b)
+        for (int k = 0; k < 8; ++k) acc[k] += (double)h[b * 8 + k] / g;
+      fprintf(stderr, "k1t waits (cycles/CTA): prod.empty %.0f | mma.acce %.0f mma.conv %.0f | "
+              "conv.accf %.0f conv.full %.0f conv.mfree %.0f | conv total %.0f\n",
+              acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6]);
+    }
+  } dbg_print{dbg, dbg_buf, grid, s};
+  CUDA_TRY(ensure_smem(k1_tc<48, 40>, smem));
+  k1_tc<48, 40><<<grid, K1T_THREADS, smem, s>>>(d, a, kg.n_items, tm[0], tm[1], tm[2], tm[3]);
+  LAUNCH_CHECK();
+  k1_tc_finalize<<<n_units, K1T_FIN_THREADS, 0, s>>>(d, a, n_units, o);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
 extern "C" int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                                  const void* y, const void* pilots, const uint64_t* seeds,
                                  int64_t first_slot, const void* state, double* sigma2_hat,
@@ -455,7 +626,8 @@ extern "C" int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int
           K1_NOISE | K1_MMSE | K1_AI, seeds ? ws_at<double>(ws, w.rng) : nullptr, seeds,
           reinterpret_cast<const unsigned char*>(state),
           state_stride_bytes(plan->dev.window_length, plan->dev.dapp_window), first_slot, n_slots};
-  int rc = launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem, s);
+  int rc = plan->k1t_nb ? launch_k1t(plan, n_units, src, o, w, ws, s)
+                        : launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem, s);
   if (rc) return rc;
   if (sigma2_hat)
     CUDA_TRY(cudaMemcpyAsync(sigma2_hat, ws_at<double>(ws, w.sigma2), n_units * sizeof(double),
@@ -494,10 +666,6 @@ static int experts_equalize_impl(const arches_plan* plan, int32_t n_streams, int
                                  arches_stream_t stream, bool rng_from_k1);
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncodeTiledFn encode_tiled() {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
@@ -656,7 +824,8 @@ extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int3
                              nullptr, ws, stream);
   if (rc) return rc;
   rc = experts_equalize_impl(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
-                             state, h_mmse, h_ai, tel, ws, stream, true);
+                             state, h_mmse, h_ai, tel, ws, stream,
+                             /* RNG side products from K1 */ true);
   if (rc) return rc;
   return arches_kpm_scan(plan, n_streams, n_slots, tel, regime, tree, state, kpm, msg_log,
                          msg_count, msg_cap, stream);

@@ -146,6 +146,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase), "r"(0x10000u)
       : "memory");
 }
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITS_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -166,4 +175,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Work split: CTA b owns the contiguous item range [b*n/G, (b+1)*n/G), so a
+// CTA walks the tiles of one unit in order and its threads keep their
+// telemetry sums in registers across them; a unit's sums are flushed once per
+// (CTA, unit) segment, at the segment's first tile.  K3 adds the segments.
+__host__ __device__ inline bool k2_segment_start(int item, int n_tiles, int n_items, int G) {
+  if (item % n_tiles == 0) return true;
+  const long long b = ((long long)item * G + n_items - 1) / n_items;  // ceil
+  return b < G && (b * n_items) / G == item;
 }

@@ -80,9 +80,6 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 // byte offset of element (row, kappa) of a K-major SWIZZLE_NONE operand with
 // `groups` 8-row groups per 8-wide K block
@@ -226,16 +223,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
       "l"(policy)
       : "memory");
-}
-
-// Work split: CTA b owns the contiguous item range [b*n/G, (b+1)*n/G), so a
-// CTA walks the tiles of one unit in order and its threads keep their
-// telemetry sums in registers across them; a unit's sums are flushed once per
-// (CTA, unit) segment, at the segment's first tile.  K3 adds the segments.
-__host__ __device__ inline bool k2_segment_start(int item, int n_tiles, int n_items, int G) {
-  if (item % n_tiles == 0) return true;
-  const long long b = ((long long)item * G + n_items - 1) / n_items;  // ceil
-  return b < G && (b * n_items) / G == item;
 }
 
 template <int NA, int ND, bool kStd, bool kTmap>

@@ -109,8 +109,79 @@ ARCHES_HD uint64_t blake2b64(const uint8_t* msg, int len) {
   return h0 ^ v[0] ^ v[8];
 }
 
+// BLAKE2b-64 of a message of len <= 32 bytes held in four little-endian words
+// (register-only form: rounds unrolled, message schedule resolved at compile time)
+#ifdef __CUDACC__
+__device__ __forceinline__ uint64_t blake2b64_short(const uint64_t m0, const uint64_t m1,
+                                                    const uint64_t m2, const uint64_t m3, int len) {
+  constexpr uint8_t sg[12][16] = {
+      {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+      {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+      {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4},
+      {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+      {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13},
+      {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+      {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11},
+      {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+      {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5},
+      {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+      {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+      {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+  uint64_t m[16] = {m0, m1, m2, m3, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const uint64_t h0 = 0x6a09e667f3bcc908ull ^ 0x01010008ull;
+  uint64_t v[16] = {h0, 0xbb67ae8584caa73bull, 0x3c6ef372fe94f82bull, 0xa54ff53a5f1d36f1ull,
+                    0x510e527fade682d1ull, 0x9b05688c2b3e6c1full, 0x1f83d9abfb41bd6bull,
+                    0x5be0cd19137e2179ull, 0x6a09e667f3bcc908ull, 0xbb67ae8584caa73bull,
+                    0x3c6ef372fe94f82bull, 0xa54ff53a5f1d36f1ull, 0x510e527fade682d1ull,
+                    0x9b05688c2b3e6c1full, 0x1f83d9abfb41bd6bull, 0x5be0cd19137e2179ull};
+  v[12] ^= (uint64_t)len;
+  v[14] = ~v[14];
+#pragma unroll
+  for (int r = 0; r < 12; ++r) {
+    b2_g(v, 0, 4, 8, 12, m[sg[r][0]], m[sg[r][1]]);
+    b2_g(v, 1, 5, 9, 13, m[sg[r][2]], m[sg[r][3]]);
+    b2_g(v, 2, 6, 10, 14, m[sg[r][4]], m[sg[r][5]]);
+    b2_g(v, 3, 7, 11, 15, m[sg[r][6]], m[sg[r][7]]);
+    b2_g(v, 0, 5, 10, 15, m[sg[r][8]], m[sg[r][9]]);
+    b2_g(v, 1, 6, 11, 12, m[sg[r][10]], m[sg[r][11]]);
+    b2_g(v, 2, 7, 8, 13, m[sg[r][12]], m[sg[r][13]]);
+    b2_g(v, 3, 4, 9, 14, m[sg[r][14]], m[sg[r][15]]);
+  }
+  return h0 ^ v[0] ^ v[8];
+}
+
+// _lcid4_jitter(slot) without byte buffers: "lcid4:" + decimal digits packed
+// straight into the message words
+__device__ __forceinline__ double lcid4_jitter_fast(uint64_t slot) {
+  int nd = 1;
+  for (uint64_t t = slot / 10ull; t; t /= 10ull) ++nd;
+  uint64_t w0 = 0x3a346469636cull, w1 = 0, w2 = 0, w3 = 0;  // "lcid4:" little-endian
+  uint64_t x = slot;
+#pragma unroll
+  for (int k = 0; k < 20; ++k) {  // digit k from the right sits at byte 6 + nd - 1 - k
+    if (k < nd) {
+      const uint64_t dgt = x % 10ull;
+      x /= 10ull;
+      const int pos = 6 + nd - 1 - k;
+      const uint64_t val = (uint64_t)('0' + (int)dgt) << (8 * (pos & 7));
+      const int wd = pos >> 3;
+      w0 |= wd == 0 ? val : 0ull;
+      w1 |= wd == 1 ? val : 0ull;
+      w2 |= wd == 2 ? val : 0ull;
+      w3 |= wd == 3 ? val : 0ull;
+    }
+  }
+  const uint64_t h = blake2b64_short(w0, w1, w2, w3, 6 + nd);
+  const double xd = __ull2double_rn(h);
+  return __dsub_rn(__dmul_rn(xd * (1.0 / 18446744073709551616.0), 2.0), 1.0);
+}
+#endif
+
 // _lcid4_jitter(slot): blake2b64("lcid4:<slot>") / 2^64 * 2 - 1
 ARCHES_HD double lcid4_jitter(uint64_t slot) {
+#ifdef __CUDA_ARCH__
+  return lcid4_jitter_fast(slot);
+#endif
   uint8_t buf[32];
   const char* pre = "lcid4:";
   int n = 0;
