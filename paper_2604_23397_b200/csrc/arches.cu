@@ -19,6 +19,7 @@
 #include "k_analyze_tc.cuh"
 #include "k_control.cuh"
 #include "k_control_warp.cuh"
+#include "k_control_block.cuh"
 #include "k_synth_eq.cuh"
 #include "k_synth_tc.cuh"
 #include "rng.cuh"
@@ -789,7 +790,7 @@ extern "C" int arches_kpm_scan(const arches_plan* plan, int32_t n_streams, int32
     return set_err(ARCHES_E_CONTRACT, "oracle policy needs the regime timeline");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   K4Args a{tel, regime, tree, state, kpm, msg_log, msg_count, msg_cap, n_streams, n_slots};
-  k4_kpm_scan_warp<<<n_streams, 32, 0, s>>>(plan->dev, a);
+  k4_kpm_scan_block<<<n_streams, K4B_THREADS, 0, s>>>(plan->dev, a);
   LAUNCH_CHECK();
   return ARCHES_OK;
 }
