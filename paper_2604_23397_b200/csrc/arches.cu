@@ -378,7 +378,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     d.num_sms = sms > 0 ? sms : 148;
     const char* pf = getenv("ARCHES_K2_PREFETCH");
-    d.pf_dist = pf ? atoi(pf) : 0;
+    d.pf_dist = pf ? atoi(pf) : 0;  // measured: no gain at 1-3 (K2 is not HBM-latency bound)
   }
 
   // ---- K1 launch geometry

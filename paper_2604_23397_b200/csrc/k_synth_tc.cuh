@@ -419,6 +419,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       issue_tma(un, tn, buf ^ 1);
       load_b(un, tn, cv);
     }
+    if constexpr (kTmap) {
+      // L2 prefetch pf_dist items ahead: the shared-memory stages hold one item
+      // in flight, the L2 holds the next ones (tensor-map prefetch, one
+      // instruction per operand)
+      const int pf = item + 1 + P.pf_dist;
+      if (P.pf_dist > 0 && threadIdx.x == 32 && pf < hi) {
+        const int pu = pf / n_tiles, pt = pf - pu * n_tiles;
+        asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tm_y)), "r"(pt * 2 * ARCHES_TILE), "r"(0), "r"(pu)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tm_x)), "r"(pt * 2 * ARCHES_TILE), "r"(0), "r"(pu)
+                     : "memory");
+      }
+    }
     // ---- this expert's synthesised taps
     mbar_wait(&s_mma[buf], ph);
     tc_fence_after();

@@ -1,7 +1,8 @@
-"""The warp-parallel K4 scan equals the one-thread-per-stream restatement
+"""The block-parallel K4 scan equals the one-thread-per-stream restatement
 (both checked against the reference by test_engine_gpu) on randomised
 telemetry, for windows shorter and longer than a warp, every policy and both
-execution modes, across several batches."""
+execution modes, across several batches, batches longer than one 256-slot
+chunk, and BASELINE config D (policy stress: 1024 cells per slot boundary)."""
 import numpy as np
 import pytest
 
@@ -39,7 +40,18 @@ def tree_on_mac(cut):
 @pytest.mark.parametrize("window,period,dwin,timeout", [(100, 100, 100, None), (5, 3, 7, 2000.0),
                                                        (1, 1, 1, None), (40, 17, 33, 9000.0)])
 @pytest.mark.parametrize("em", [ExecutionMode.CONCURRENT, ExecutionMode.SELECTED_ONLY])
-def test_warp_scan_equals_sequential(policy, window, period, dwin, timeout, em):
+@pytest.mark.parametrize("n_streams,n_slots", [(3, 77), (2, 300)])
+def test_block_scan_equals_sequential(policy, window, period, dwin, timeout, em, n_streams, n_slots):
+    _compare_scans(policy, window, period, dwin, timeout, em, n_streams, n_slots, batches=3)
+
+
+def test_policy_stress_1024_cells():
+    """Config D: 1024 cells, reference dApp defaults (100-slot windows, a
+    decision every 100 slots), depth-2 tree, one batch of 250 slots per cell."""
+    _compare_scans("tree", 100, 100, 100, None, ExecutionMode.CONCURRENT, 1024, 250, batches=2)
+
+
+def _compare_scans(policy, window, period, dwin, timeout, em, C_, S, batches):
     import torch
     rng = np.random.default_rng(window * 1000 + period)
     geo = SlotGeometry(n_ant=2, n_prb=4)
@@ -47,7 +59,6 @@ def test_warp_scan_equals_sequential(policy, window, period, dwin, timeout, em):
     dcfg = DappConfig(decision_period_slots=period, window_length_slots=dwin,
                       failsafe_timeout_us=timeout)
     plan = ArchesPlan(geo, 1.25, pcfg, em, policy, dcfg)
-    C_, S = 3, 77
     L = _lib.lib()
     dev = torch.device("cuda")
     tree = torch.frombuffer(bytearray(bytes(to_device_struct(tree_on_mac(6.5e6 * 8 / 1e6 * 1e-3)))),
@@ -60,7 +71,7 @@ def test_warp_scan_equals_sequential(policy, window, period, dwin, timeout, em):
         kpms.append(torch.zeros(C_ * S * 104, dtype=torch.uint8, device=dev))
         logs.append(torch.zeros(C_ * 512 * 24, dtype=torch.uint8, device=dev))
         counts.append(torch.zeros(C_, dtype=torch.int32, device=dev))
-    for batch in range(3):
+    for batch in range(batches):
         tel = random_tel(rng, C_ * S, pcfg.mcs_table)
         # make the MAC rate regime-dependent so the tree flips
         reg = (rng.random(C_ * S) < (0.9 if batch % 2 else 0.1)).astype(np.int8)
