@@ -68,6 +68,7 @@ struct arches_plan {
   size_t k1_full_smem;
   size_t k2_smem;
   size_t k2_tc_smem;  // 0: tensor-core K2 not applicable to this plan
+  int k2_groups;      // > 1: tensor-core K2 over antenna groups of 4 (massive MIMO)
   void* dev_tables;
 };
 
@@ -457,19 +458,25 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
   P->k2_smem = ((size_t)(d.A + 1) * d.T * ARCHES_TILE + (size_t)d.nbt_max * AD * 8 +
                 (size_t)AD * d.trunc) * sizeof(float2);
   {
-    // tcgen05 K2: n_ant in {1,2,4} (padded), tiles inside one MMSE block
-    const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : d.A <= 4 ? 4 : 0;
+    // tcgen05 K2: n_ant in {1,2,4} (padded), tiles inside one MMSE block; more
+    // antennas (a multiple of 4, NR 0/5/10 DMRS pattern) run in groups of 4
+    const bool std_pat = d.T == 14 && d.D == 3 && d.dsym[0] == 0 && d.dsym[1] == 5 && d.dsym[2] == 10;
+    const bool grp = d.A > 4 && d.A % 4 == 0 && std_pat;
+    const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : d.A <= 4 ? 4 : grp ? 4 : 0;
     const bool tile_ok = d.n_blocks == 1 || (d.block % ARCHES_TILE) == 0;
     size_t sm = 0;
     if (na && tile_ok && 16 * d.tc_kb <= 128 && !getenv("ARCHES_DISABLE_TC")) {
       const int R = 2 * na * d.D, ncol = ((2 * R + 15) / 16) * 16, ng = ncol / 8;
       const int n_b = (ncol / 2) * 4 * d.tc_kb;  // B entries: <= 2 per thread of 512
-      sm = 2 * (size_t)(d.A + 1) * d.T * ARCHES_TILE * sizeof(float2) + 4 * (size_t)d.tc_kb * ng * 256;
+      const int as = grp ? 4 : d.A;               // antennas per stage
+      sm = 2 * (size_t)(as + 1) * d.T * ARCHES_TILE * sizeof(float2) + 4 * (size_t)d.tc_kb * ng * 256;
+      if (grp) sm += (size_t)21 * TC_THREADS * sizeof(float);  // MRC sums across groups
       if (sm > 227 * 1024 || n_b > 2 * TC_THREADS || ncol > 64) sm = 0;
     }
     P->k2_tc_smem = sm;
+    P->k2_groups = grp && sm ? d.A / 4 : 1;
   }
-  if (P->k2_smem > 200 * 1024) {
+  if (P->k2_smem > 200 * 1024 && !(P->k2_tc_smem && P->k2_groups > 1)) {
     cudaFree(buf);
     delete P;
     return set_err(ARCHES_E_CONFIG, "K2 tile does not fit shared memory (n_ant too large)");
@@ -683,12 +690,14 @@ static EncodeTiledFn encode_tiled() {
 
 // [units][rows][N] complex64 viewed as fp32 [units][rows][2N]; box = one
 // 128-subcarrier tile of all rows of one unit
-static bool make_row_tmap(CUtensorMap* m, const void* base, int N, int rows, int units) {
+static bool make_row_tmap(CUtensorMap* m, const void* base, int N, int rows, int units,
+                          int box_rows = 0) {
   EncodeTiledFn enc = encode_tiled();
-  if (!enc || (N & 1) || rows > 256 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  if (box_rows <= 0) box_rows = rows;
+  if (!enc || (N & 1) || box_rows > 256 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)2 * N, (cuuint64_t)rows, (cuuint64_t)units};
   const cuuint64_t strides[2] = {(cuuint64_t)8 * N, (cuuint64_t)8 * N * rows};
-  const cuuint32_t box[3] = {2 * ARCHES_TILE, (cuuint32_t)rows, 1};
+  const cuuint32_t box[3] = {2 * ARCHES_TILE, (cuuint32_t)box_rows, 1};
   const cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -697,8 +706,9 @@ static bool make_row_tmap(CUtensorMap* m, const void* base, int N, int rows, int
 
 static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cudaStream_t s) {
   const PlanDev& d = P->dev;
-  const int n_items = n_units * d.n_tiles;
-  const int grid = std::min(n_items, d.num_sms);  // persistent: one CTA per SM
+  const int ngrp = P->k2_groups;
+  const int n_items = n_units * d.n_tiles * ngrp;
+  const int grid = std::min(n_units * d.n_tiles, d.num_sms);  // persistent: one CTA per SM
   const size_t smem = P->k2_tc_smem;
   const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : 4;
   const bool std_pat = d.T == 14 && d.D == 3 && d.dsym[0] == 0 && d.dsym[1] == 5 && d.dsym[2] == 10;
@@ -706,18 +716,22 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
   memset(&tm_y, 0, sizeof(tm_y));
   memset(&tm_x, 0, sizeof(tm_x));
   const bool tmap = getenv("ARCHES_K2_NO_TMAP") == nullptr &&
-                    make_row_tmap(&tm_y, a.y, d.N, d.A * d.T, n_units) &&
+                    make_row_tmap(&tm_y, a.y, d.N, d.A * d.T, n_units, ngrp > 1 ? 4 * d.T : 0) &&
                     make_row_tmap(&tm_x, a.tx, d.N, d.T, n_units);
-#define K2TC_LAUNCH(NA_, ND_, STD_)                                                          \
+#define K2TC_LAUNCH_G(NA_, ND_, STD_, GRP_)                                                  \
   {                                                                                          \
-    auto kern = tmap ? k2_tc<NA_, ND_, STD_, true> : k2_tc<NA_, ND_, STD_, false>;           \
+    auto kern = tmap ? k2_tc<NA_, ND_, STD_, true, GRP_> : k2_tc<NA_, ND_, STD_, false, GRP_>; \
     CUDA_TRY(ensure_smem(kern, smem));                                                       \
     kern<<<grid, TC_THREADS, smem, s>>>(d, a, n_items, tm_y, tm_x);                          \
     LAUNCH_CHECK();                                                                          \
-    k3_finalize<<<(n_units * 32 + K3_THREADS - 1) / K3_THREADS, K3_THREADS, 0, s>>>(d, a, n_units, n_items, grid); \
+    /* K3 locates the (CTA, unit) segments in tile units */                                  \
+    k3_finalize<<<(n_units * 32 + K3_THREADS - 1) / K3_THREADS, K3_THREADS, 0, s>>>(         \
+        d, a, n_units, n_items / ngrp, grid);                                                \
     LAUNCH_CHECK();                                                                          \
     return ARCHES_OK;                                                                        \
   }
+#define K2TC_LAUNCH(NA_, ND_, STD_) K2TC_LAUNCH_G(NA_, ND_, STD_, false)
+  if (ngrp > 1) K2TC_LAUNCH_G(4, 3, true, true)  /* massive MIMO: groups of 4 antennas */
 #define K2TC_CASE(NA_, ND_)                                                                  \
   if (na == NA_ && d.D == ND_) K2TC_LAUNCH(NA_, ND_, false)
   if (std_pat && d.A == 4) K2TC_LAUNCH(4, 3, true)  /* kStd: exact n_ant, NR 0/5/10 pattern */
@@ -728,6 +742,7 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
   K2TC_CASE(4, 1) K2TC_CASE(4, 2) K2TC_CASE(4, 3) K2TC_CASE(4, 4)
 #undef K2TC_CASE
 #undef K2TC_LAUNCH
+#undef K2TC_LAUNCH_G
   return launch_k2<2>(P, n_units, a, s);
 }
 

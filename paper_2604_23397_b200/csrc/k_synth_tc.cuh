@@ -225,7 +225,60 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <int NA, int ND, bool kStd, bool kTmap>
+// antenna-group form of eq_std_half (massive-MIMO plans, 4 antennas per
+// group): MRC numerator / denominator per symbol accumulate in shared memory
+// (g[0..6] = Re num, g[7..13] = Im num, g[14..20] = den, stride TC_THREADS)
+// across the groups of one tile; the last group forms x_hat and the SINR sums.
+template <int NA, int ND, int H, bool SXX>
+__device__ __forceinline__ void eq_grp_half(const float2 (&h)[NA][ND], const float2* yrow,
+                                            const float2* xrow, float modd, float nv, float* g,
+                                            bool first, bool last, float& sre, float& sim,
+                                            float& syy, float& sxx) {
+  constexpr int kSym[2][7] = {{0, 1, 2, 3, 4, 5, 10}, {6, 7, 8, 9, 11, 12, 13}};
+#pragma unroll
+  for (int tt = 0; tt < 7; ++tt) {
+    const int t = kSym[H][tt];
+    float wt[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) wt[d] = std_tw(t, d);
+    float2 num = first ? make_float2(0.f, 0.f) : make_float2(g[tt * TC_THREADS], g[(7 + tt) * TC_THREADS]);
+    float den = first ? 0.f : g[(14 + tt) * TC_THREADS];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      const float2 yv = yrow[(size_t)(a * 14 + t) * ARCHES_TILE];
+      float2 hn = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        if (wt[d] != 0.f) {
+          hn.x = fmaf(wt[d], h[a][d].x, hn.x);
+          hn.y = fmaf(wt[d], h[a][d].y, hn.y);
+        }
+      }
+      num.x = fmaf(hn.x, yv.x, fmaf(hn.y, yv.y, num.x));
+      num.y = fmaf(hn.x, yv.y, fmaf(-hn.y, yv.x, num.y));
+      den = fmaf(hn.x, hn.x, fmaf(hn.y, hn.y, den));
+    }
+    if (!last) {
+      g[tt * TC_THREADS] = num.x;
+      g[(7 + tt) * TC_THREADS] = num.y;
+      g[(14 + tt) * TC_THREADS] = den;
+      continue;
+    }
+    const float2 x = xrow[(size_t)t * ARCHES_TILE];
+    const bool dm = (t == 0 || t == 5 || t == 10);
+    const float m = dm ? modd : 1.f;
+    float inv;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(den + nv));
+    inv *= m;
+    const float hr = num.x * inv, hi = num.y * inv;
+    sre = fmaf(x.x, hr, fmaf(x.y, hi, sre));
+    sim = fmaf(x.x, hi, fmaf(-x.y, hr, sim));
+    syy = fmaf(hr, hr, fmaf(hi, hi, syy));
+    if (SXX) sxx = fmaf(m * x.x, x.x, fmaf(m * x.y, x.y, sxx));
+  }
+}
+
+template <int NA, int ND, bool kStd, bool kTmap, bool kGrp = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k2_tc(const PlanDev P, const K2Args args, const int n_items,
           const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ CUtensorMap tm_x) {
@@ -249,33 +302,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int AD = P.A * ND;
   const int n_tiles = P.n_tiles;
   const int G = gridDim.x;
-  const int lo = (int)((long long)blockIdx.x * n_items / G);
-  const int hi = (int)((long long)(blockIdx.x + 1) * n_items / G);
+  // antenna groups (massive MIMO): a work item is (unit, tile, group of NA
+  // antennas); CTA ranges are whole tiles so the MRC sums stay on one CTA
+  const int ngrp = kGrp ? P.A / NA : 1;
+  const int AS = kGrp ? NA : P.A;  // antennas per shared-memory stage
+  const int n_titems = n_items / ngrp;
+  const int lo = (int)((long long)blockIdx.x * n_titems / G) * ngrp;
+  const int hi = (int)((long long)(blockIdx.x + 1) * n_titems / G) * ngrp;
   const uint32_t b_bytes = (uint32_t)KB * NG * 256;
-  const size_t stage_elems = (size_t)(P.A + 1) * T * ARCHES_TILE;
+  const size_t stage_elems = (size_t)(AS + 1) * T * ARCHES_TILE;
   const size_t coef_stride = coef_floats2(P);
   float2* sYX = reinterpret_cast<float2*>(sm);                               // [2][stage]
   unsigned char* sB = sm + 2 * stage_elems * sizeof(float2);                 // [2][hi | lo]
+  float* gacc = reinterpret_cast<float*>(sB + 4 * (size_t)KB * NG * 256) + threadIdx.x;  // [21][512] (kGrp)
   const int n_all = (NCOL / 2) * L4;                                         // B entries
   const uint32_t ACC0 = 128;                                                 // TMEM columns
   // this thread's <= 2 B entries (output column pair r, tap l): source offsets
   // inside a unit's coefficients, rotation index, shared-memory offsets
-  int boff[2], roff[2];
+  int boff[2], roff[2], gstr[2];
   bool bmm[2];
   uint32_t o0[2], o1[2];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int e = threadIdx.x + q * TC_THREADS;
-    boff[q] = -1; roff[q] = 0; bmm[q] = false; o0[q] = o1[q] = 0;
+    boff[q] = -1; roff[q] = 0; bmm[q] = false; o0[q] = o1[q] = 0; gstr[q] = 0;
     if (e < n_all) {
       const int r = e / L4, l = e - r * L4;
       o0[q] = kmaj_off(2 * r, 2 * l, NG);
       o1[q] = kmaj_off(2 * r + 1, 2 * l, NG);
       if (r < NA * ND) {
-        if (r < AD && l < P.trunc) { boff[q] = AD * P.n_blocks * 8 + r * P.trunc + l; roff[q] = l; }
+        if (r < AD && l < P.trunc) {
+          boff[q] = AD * P.n_blocks * 8 + r * P.trunc + l; roff[q] = l; gstr[q] = NA * ND * P.trunc;
+        }
       } else if (r < R) {
         const int ad = r - NA * ND;
-        if (ad < AD && l < 8) { boff[q] = ad * P.n_blocks * 8 + l; roff[q] = L4 + l; bmm[q] = true; }
+        if (ad < AD && l < 8) {
+          boff[q] = ad * P.n_blocks * 8 + l; roff[q] = L4 + l; bmm[q] = true; gstr[q] = NA * ND * P.n_blocks * 8;
+        }
       }
     }
   }
@@ -298,37 +361,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = s_tmem;
   const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
 
-  auto issue_tma = [&](int u, int tile, int stage) {
+  auto issue_tma = [&](int u, int tile, int gr, int stage) {
     const uint64_t pol = l2_evict_first_policy();
     float2* dst = sYX + (size_t)stage * stage_elems;
-    if constexpr (kTmap) {  // thread 0: two tensor copies (y rows, tx rows)
+    const bool with_x = gr == ngrp - 1;  // tx rows: needed by the last group only
+    if constexpr (kTmap) {  // thread 0: two tensor copies (y rows of the group, tx rows)
       if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(&s_full[stage], (uint32_t)(stage_elems * sizeof(float2)));
-        tma_load_3d(dst, &tm_y, tile * 2 * ARCHES_TILE, 0, u, &s_full[stage], pol);
-        tma_load_3d(dst + (size_t)P.A * T * ARCHES_TILE, &tm_x, tile * 2 * ARCHES_TILE, 0, u,
-                    &s_full[stage], pol);
+        const size_t ybytes = (size_t)AS * T * ARCHES_TILE * sizeof(float2);
+        mbar_arrive_expect_tx(&s_full[stage], (uint32_t)(with_x ? stage_elems * sizeof(float2) : ybytes));
+        tma_load_3d(dst, &tm_y, tile * 2 * ARCHES_TILE, gr * AS * T, u, &s_full[stage], pol);
+        if (with_x)
+          tma_load_3d(dst + (size_t)AS * T * ARCHES_TILE, &tm_x, tile * 2 * ARCHES_TILE, 0, u,
+                      &s_full[stage], pol);
       }
     } else if (lane == 0) {  // lane 0 of every warp: rows r = warp (mod 16)
       const int k0 = tile * ARCHES_TILE;
       const uint32_t rowb = (uint32_t)min(ARCHES_TILE, P.N - k0) * sizeof(float2);
-      const int rows = (P.A + 1) * T;
+      const int rows = AS * T + (with_x ? T : 0);
       const int nw = TC_THREADS / 32;
       const int mine = (rows - warp + nw - 1) / nw;
       mbar_arrive_expect_tx(&s_full[stage], rowb * (uint32_t)mine);
       for (int r = warp; r < rows; r += nw) {
-        const float2* src = (r < P.A * T) ? args.y + ((size_t)u * P.A * T + r) * P.N + k0
-                                          : args.tx + ((size_t)u * T + (r - P.A * T)) * P.N + k0;
+        const float2* src = (r < AS * T) ? args.y + ((size_t)u * P.A * T + (size_t)gr * AS * T + r) * P.N + k0
+                                         : args.tx + ((size_t)u * T + (r - AS * T)) * P.N + k0;
         bulk_g2s(dst + (size_t)r * ARCHES_TILE, src, rowb, &s_full[stage], pol);
       }
     }
   };
-  auto load_b = [&](int u, int tile, float2 (&cv)[2]) {  // coefficients rotated to the tile
+  auto load_b = [&](int u, int tile, int gr, float2 (&cv)[2]) {  // coefficients rotated to the tile
     const float2* cu = args.coef + (size_t)u * coef_stride;
     const float2* rot = P.tc_rot + (size_t)tile * (L4 + 8);
     const int bo = P.n_blocks == 1 ? 0 : min(tile * ARCHES_TILE / P.block, P.n_blocks - 1) * 8;
 #pragma unroll
     for (int q = 0; q < 2; ++q)
-      cv[q] = boff[q] >= 0 ? cmul(__ldg(&cu[boff[q] + (bmm[q] ? bo : 0)]), __ldg(&rot[roff[q]]))
+      cv[q] = boff[q] >= 0 ? cmul(__ldg(&cu[boff[q] + (bmm[q] ? bo : 0) + gr * gstr[q]]), __ldg(&rot[roff[q]]))
                            : make_float2(0.f, 0.f);
   };
   auto write_b = [&](int buf, const float2 (&cv)[2]) {
@@ -364,10 +430,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     umma_commit(&s_mma[buf]);
   };
 
-  int u = lo / n_tiles, tile = lo - u * n_tiles;
+  int u = (lo / ngrp) / n_tiles, tile = (lo / ngrp) - u * n_tiles, gr = 0;
   // ---- prologue: A operand (twiddle rows) -> TMEM, item 0 data + B(0) + MMA(0)
   if (lo < hi) {
-    issue_tma(u, tile, 0);
+    issue_tma(u, tile, 0, 0);
     if (warp < 4) {
       const float4* arow = reinterpret_cast<const float4*>(P.tc_a) + (size_t)j * (KB * 4);
       for (int c = 0; c < KB; ++c) {
@@ -393,7 +459,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     float2 cv[2];
-    load_b(u, tile, cv);
+    load_b(u, tile, 0, cv);
     write_b(0, cv);
     tc_fence_before();
     __syncthreads();
@@ -407,8 +473,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   for (int item = lo, i = 0; item < hi; ++item, ++i) {
     const int buf = i & 1, ph = (i >> 1) & 1;
     const bool has_next = item + 1 < hi;
-    const bool last_tile = tile + 1 == n_tiles;
-    const int un = last_tile ? u + 1 : u, tn = last_tile ? 0 : tile + 1;
+    const bool last_grp = gr + 1 == ngrp;
+    const bool last_tile = tile + 1 == n_tiles && last_grp;  // last item of the unit
+    const int gn = last_grp ? 0 : gr + 1;
+    const int tn = last_grp ? (tile + 1 == n_tiles ? 0 : tile + 1) : tile;
+    const int un = last_tile ? u + 1 : u;
     const bool flush = last_tile || !has_next;
     const int k0 = tile * ARCHES_TILE;
     const int kk = k0 + j;
@@ -416,15 +485,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---- next item's data + coefficients in flight during this item's work
     float2 cv[2];
     if (has_next) {
-      issue_tma(un, tn, buf ^ 1);
-      load_b(un, tn, cv);
+      issue_tma(un, tn, gn, buf ^ 1);
+      load_b(un, tn, gn, cv);
     }
     if constexpr (kTmap) {
       // L2 prefetch pf_dist items ahead: the shared-memory stages hold one item
       // in flight, the L2 holds the next ones (tensor-map prefetch, one
       // instruction per operand)
       const int pf = item + 1 + P.pf_dist;
-      if (P.pf_dist > 0 && threadIdx.x == 32 && pf < hi) {
+      if (!kGrp && P.pf_dist > 0 && threadIdx.x == 32 && pf < hi) {
         const int pu = pf / n_tiles, pt = pf - pu * n_tiles;
         asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
                          reinterpret_cast<uint64_t>(&tm_y)), "r"(pt * 2 * ARCHES_TILE), "r"(0), "r"(pu)
@@ -448,7 +517,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         h[a][d] = make_float2(vals[2 * (a * ND + d)], vals[2 * (a * ND + d) + 1]);
     float2* hout = ex ? args.h_mmse : args.h_ai;
     if (valid && half == 0 && hout) {  // half 0 stores the expert output ...
-      float2* o = hout + (size_t)u * AD * P.N + kk;
+      float2* o = hout + ((size_t)u * AD + (size_t)gr * NA * ND) * P.N + kk;
 #pragma unroll
       for (int a = 0; a < NA; ++a)
         if (kStd || a < P.A)
@@ -472,8 +541,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (valid) {
       const float modd = (kk & 1) ? 1.f : 0.f;  // pilot REs: even k on DMRS symbols
       const float2* yrow = sYX + (size_t)buf * stage_elems + j;
-      const float2* xrow = yrow + (size_t)P.A * T * ARCHES_TILE;
-      if (kStd) {  // compile-time symbol half and expert: weights and pilot symbols fold
+      const float2* xrow = yrow + (size_t)AS * T * ARCHES_TILE;
+      if (kGrp) {  // antenna groups: MRC sums across the tile's groups, finalised at the last
+        const bool first = gr == 0, last = gr + 1 == ngrp;
+        if (half == 0) {
+          if (ex == 0) eq_grp_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
+          else         eq_grp_half<NA, ND, 0, false>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
+        } else {
+          if (ex == 0) eq_grp_half<NA, ND, 1, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
+          else         eq_grp_half<NA, ND, 1, false>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
+        }
+      } else if (kStd) {  // compile-time symbol half and expert: weights and pilot symbols fold
         if (half == 0) {
           if (ex == 0) eq_std_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
           else         eq_std_half<NA, ND, 0, false>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
@@ -543,6 +621,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     u = un;
     tile = tn;
+    gr = gn;
   }
   tc_fence_before();
   __syncthreads();
