@@ -6,13 +6,18 @@ per-slot latency", workload configs[1]: single cell, 273 PRB, 4 RX, 1 layer,
 good/poor regimes alternating every slot so the oracle policy flips the expert
 every slot (concurrent execution, mode applied at the next boundary).
 
-A step = one pass of the hot path (K1 LS+analysis -> K2 experts+switch
-telemetry+equaliser+KPM candidates -> K4 KPM windows/control) over a batch of
-S consecutive slots of each rank's cell.  Ranks process independent cells
-(seed = 1000 + rank): weak scaling, no collective on the data path, one
-all_reduce(MAX) of the elapsed time at the end.
+A step = one pass of the hot path (K1 LS + delay-domain analysis on tcgen05 ->
+K1 finalize (sigma2, taps, RNG) -> K2 experts + switch telemetry + equaliser on
+tcgen05 -> K3 KPM candidates -> K4 KPM windows / control plane) over a batch
+of S consecutive slots of each of the rank's streams.  Ranks process
+independent cells (seeds 1000 + rank*streams + k): weak scaling, no collective
+on the data path, one all_reduce(MAX) of the elapsed time at the end.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--slots S] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--slots S] [--streams C]
+                  [--n-prb P] [--n-ant A] [--impl ours|reference]
+
+Defaults are config B (the headline).  Config C per rank: --streams 16 --slots 16
+(8 cells x 2 layers); config E: --n-ant 64 --streams 4 --slots 8.
 
 Prints ONE JSON line (rank 0).
 """
@@ -47,6 +52,8 @@ def parse():
     ap.add_argument("--slots", type=int, default=256, help="slots per step per rank")
     ap.add_argument("--n-prb", type=int, default=273)
     ap.add_argument("--n-ant", type=int, default=4)
+    ap.add_argument("--streams", type=int, default=1,
+                    help="independent single-layer streams per rank (cells x layers; configs C/E)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--latency-slots", type=int, default=400)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -157,6 +164,15 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ inputs
+def make_stream_inputs(n_prb, n_ant, S, seeds):
+    """One scene per stream (seed per stream); stream-major unit order."""
+    outs = [make_inputs(n_prb, n_ant, S, sd) for sd in seeds]
+    geo, scens = outs[0][0], outs[0][1]
+    pil = np.stack([o[2] for o in outs])
+    return (geo, scens, pil, np.concatenate([o[3] for o in outs]), np.concatenate([o[4] for o in outs]),
+            np.concatenate([o[5] for o in outs]), np.concatenate([o[6] for o in outs]))
+
+
 def make_inputs(n_prb, n_ant, S, seed):
     from paper_2604_23397_b200.geometry import SlotGeometry, default_scenarios
     from paper_2604_23397_b200.scene import CellScene
@@ -178,6 +194,17 @@ def make_inputs(n_prb, n_ant, S, seed):
 
 
 # ------------------------------------------------------------------ ours
+def workload_name(a):
+    if a.n_ant == 4 and a.streams == 1:
+        return ("B: 1 cell/rank, 273 PRB, 4 RX, 1 layer, good/poor alternating every slot, oracle "
+                "policy, concurrent experts")
+    if a.n_ant == 4:
+        return (f"C: {a.streams} streams (cells x layers)/rank, {a.n_prb} PRB, 4 RX, good/poor "
+                "alternating, oracle policy, concurrent experts")
+    return (f"E: {a.streams} layer streams/rank, {a.n_prb} PRB, {a.n_ant} RX (massive MIMO), "
+            "good/poor alternating, oracle policy, concurrent experts")
+
+
 def run_ours(a, rank, world, dist):
     import torch
     from paper_2604_23397_b200 import _lib
@@ -185,15 +212,16 @@ def run_ours(a, rank, world, dist):
     from paper_2604_23397_b200.engine import ArchesPlan, SlotEngine
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    S, K, W = a.slots, a.steps, max(3, a.warmup)
-    seed = 1000 + rank
-    geo, scens, pil, y, tx, nv, reg = make_inputs(a.n_prb, a.n_ant, S, seed)
+    S, K, W, C = a.slots, a.steps, max(3, a.warmup), a.streams
+    seeds = [1000 + rank * C + k for k in range(C)]
+    geo, scens, pil, y, tx, nv, reg = make_stream_inputs(a.n_prb, a.n_ant, S, seeds)
     A, T, N, D = geo.n_ant, geo.n_sym, geo.n_sc, geo.n_dmrs
     plan = ArchesPlan(geo, scens["good"].assumed_delay_spread, PipelineConfig(),
                       ExecutionMode.CONCURRENT, "oracle")
-    eng = SlotEngine(plan, 1, S)
-    eng.set_streams(pil[None], [seed])
+    eng = SlotEngine(plan, C, S)
+    eng.set_streams(pil, seeds)
     eng.load(y=y, tx=tx, noise_var=nv, regime=reg)
+    U = C * S  # units (stream-slots) per step
     torch.cuda.synchronize()
 
     def barrier():
@@ -230,7 +258,7 @@ def run_ours(a, rank, world, dist):
         tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
-    value = K * S * world / (t_max / 1000.0)
+    value = K * U * world / (t_max / 1000.0)
 
     # ---- per-kernel times (eager, events around each stage on the launch stream)
     L = _lib.lib()
@@ -240,15 +268,15 @@ def run_ours(a, rank, world, dist):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4 * reps)]
     for r in range(reps):
         ev[4 * r].record()
-        _lib.check(L.arches_ls_analyze(plan.handle, 1, S, _lib.ptr(eng.y), _lib.ptr(eng.pilots),
+        _lib.check(L.arches_ls_analyze(plan.handle, C, S, _lib.ptr(eng.y), _lib.ptr(eng.pilots),
                                        None, -1, _lib.ptr(eng.state), None, _lib.ptr(ws), st))
         ev[4 * r + 1].record()
-        _lib.check(L.arches_experts_equalize(plan.handle, 1, S, _lib.ptr(eng.y), _lib.ptr(eng.tx),
+        _lib.check(L.arches_experts_equalize(plan.handle, C, S, _lib.ptr(eng.y), _lib.ptr(eng.tx),
                                              _lib.ptr(eng.noise_var), _lib.ptr(eng.seeds), -1,
                                              _lib.ptr(eng.state), _lib.ptr(eng.h_mmse),
                                              _lib.ptr(eng.h_ai), _lib.ptr(eng.tel), _lib.ptr(ws), st))
         ev[4 * r + 2].record()
-        _lib.check(L.arches_kpm_scan(plan.handle, 1, S, _lib.ptr(eng.tel), _lib.ptr(eng.regime),
+        _lib.check(L.arches_kpm_scan(plan.handle, C, S, _lib.ptr(eng.tel), _lib.ptr(eng.regime),
                                      None, _lib.ptr(eng.state), _lib.ptr(eng.kpm),
                                      _lib.ptr(eng.msg_log), _lib.ptr(eng.msg_count), eng.msg_cap, st))
         ev[4 * r + 3].record()
@@ -260,8 +288,16 @@ def run_ours(a, rank, world, dist):
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     peak = float(peaks["hbm_gbs"])
-    k2_gbs = S * unit_bytes / (k2 * 1e-3) / 1e9
-    step_gbs = S * unit_bytes / (t_max / K * 1e-3) / 1e9
+    k2_gbs = U * unit_bytes / (k2 * 1e-3) / 1e9
+    step_gbs = U * unit_bytes / (t_max / K * 1e-3) / 1e9
+    k1_bytes = 8 * N * A * D  # K1 reads the DMRS rows of y (both parities of each 32-byte sector)
+    k1_gbs = U * k1_bytes / (k1 * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k2_dram_traffic.json")
+    if os.path.exists(tpath):  # dram__bytes_read + write per K2 launch, from the committed ncu capture
+        tj = json.load(open(tpath))
+        if tj.get("n_prb") == a.n_prb and tj.get("n_ant") == A and tj.get("units") == U:
+            traffic = tj["bytes_per_launch"]
 
     # ---- e2e through the public engine API: pinned host inputs -> H2D -> run -> D2H KPMs
     y_h = torch.from_numpy(y).pin_memory()
@@ -296,7 +332,7 @@ def run_ours(a, rank, world, dist):
     lat = None
     if a.latency_slots > 0:
         eng1 = SlotEngine(plan, 1, 1)
-        eng1.set_streams(pil[None], [seed])
+        eng1.set_streams(pil[:1], seeds[:1])
         eng1.load(y=y[:1], tx=tx[:1], noise_var=nv[:1], regime=reg[:1])
         for _ in range(5):
             eng1.run()
@@ -315,7 +351,8 @@ def run_ours(a, rank, world, dist):
         us = np.array([b.elapsed_time(e) * 1000.0 for b, e in evs])
         lat = {"p50_us": float(np.percentile(us, 50)), "p99_us": float(np.percentile(us, 99)),
                "max_us": float(us.max()), "slots": int(len(us)),
-               "how": "1 slot per CUDA-graph launch (K1+K2+K4), CUDA events, inputs in HBM"}
+               "how": "1 slot of one stream per CUDA-graph launch (K1, K1 finalize, K2, K3, K4), "
+                      "CUDA events, inputs in HBM"}
 
     line = None
     if rank == 0:
@@ -329,21 +366,25 @@ def run_ours(a, rank, world, dist):
             "warmup": W, "ms_per_step": t_max / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c64/f64",
             "data": "synthetic (reference TDL scene, bit-exact; S-slot pool per rank replayed each step)",
-            "config": {"workload": "B: 1 cell/rank, 273 PRB, 4 RX, 1 layer, good/poor alternating "
-                                   "every slot, oracle policy, concurrent experts",
-                       "n_prb": a.n_prb, "n_ant": a.n_ant, "slots_per_step": S,
-                       "l2": f"inputs {S * unit_bytes / 1e6:.0f} MB per step > 126 MB L2 (no flush)",
-                       "parallelism": f"dp{world} (cell per rank)"},
+            "config": {"workload": workload_name(a),
+                       "n_prb": a.n_prb, "n_ant": a.n_ant, "streams_per_rank": C, "slots_per_step": S,
+                       "l2": f"inputs {U * unit_bytes / 1e6:.0f} MB per step > 126 MB L2 (no flush)",
+                       "parallelism": f"dp{world} (cells sharded by rank)"},
             "roofline": {"bound": "hbm", "achieved": k2_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": k2_gbs / peak, "traffic": None,
-                         "kernel": "k2_synth_equalize", "algorithmic_bytes_per_unit": unit_bytes,
-                         "kernel_ms": {"k1_analyze": k1, "k2_synth_equalize": k2, "k4_kpm_scan": k4},
+                         "frac": k2_gbs / peak, "traffic": traffic,
+                         "kernel": "k2_tc (+k3_finalize): expert synthesis on tcgen05 + switch "
+                                   "telemetry + equaliser",
+                         "algorithmic_bytes_per_unit": unit_bytes, "units_per_launch": U,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                         "kernel_ms": {"k1_tc+finalize": k1, "k2_tc+k3": k2, "k4_kpm_scan_block": k4},
+                         "k1": {"achieved": k1_gbs, "frac": k1_gbs / peak,
+                                "algorithmic_bytes_per_unit": k1_bytes},
                          "step_gbs": step_gbs, "step_frac": step_gbs / peak},
             "cpu_baseline": cpu,
-            "e2e": {"value": K * S * world / (te / 1000.0), "unit": UNIT,
+            "e2e": {"value": K * U * world / (te / 1000.0), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "latency": lat,
-            "gpu_launches": 3 * K,
+            "gpu_launches": 5 * K,  # K1 + K1 finalize + K2 + K3 + K4 per step (one CUDA graph)
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -616,22 +616,52 @@ static int launch_k1t(const arches_plan* P, int n_units, const GridCombSrc& src,
   return ARCHES_OK;
 }
 
+static int launch_rng(const arches_plan* plan, int n_streams, int n_slots, const uint64_t* seeds,
+                      int64_t first_slot, const void* state, void* ws, cudaStream_t s) {
+  const int n_units = n_streams * n_slots;
+  const WsLayout w = ws_layout(plan, n_units);
+  k_rng_units<<<(n_units + 127) / 128, 128, 0, s>>>(
+      plan->dev, ws_at<double>(ws, w.rng), seeds, reinterpret_cast<const unsigned char*>(state),
+      state_stride_bytes(plan->dev.window_length, plan->dev.dapp_window), first_slot, n_slots,
+      n_units);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+static int ls_analyze_impl(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                           const void* y, const void* pilots, const uint64_t* seeds,
+                           int64_t first_slot, const void* state, double* sigma2_hat, void* ws,
+                           arches_stream_t stream, bool with_rng);
+
 extern "C" int arches_ls_analyze(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                                  const void* y, const void* pilots, const uint64_t* seeds,
                                  int64_t first_slot, const void* state, double* sigma2_hat,
                                  void* ws, arches_stream_t stream) {
+  return ls_analyze_impl(plan, n_streams, n_slots, y, pilots, seeds, first_slot, state, sigma2_hat,
+                         ws, stream, true);
+}
+
+static int ls_analyze_impl(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                           const void* y, const void* pilots, const uint64_t* seeds,
+                           int64_t first_slot, const void* state, double* sigma2_hat, void* ws,
+                           arches_stream_t stream, bool with_rng) {
   if (!plan || !y || !pilots || !ws || n_streams < 1 || n_slots < 1)
     return set_err(ARCHES_E_CONTRACT, "bad ls_analyze args");
   const int n_units = n_streams * n_slots;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const WsLayout w = ws_layout(plan, n_units);
   GridCombSrc src{reinterpret_cast<const float2*>(y), reinterpret_cast<const float2*>(pilots), n_slots};
-  CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.k1counters), 0, n_units * sizeof(unsigned int), s));
+  if (!plan->k1t_nb)  // last-CTA counters of the CUDA-core K1 (the tensor-core K1 has none)
+    CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.k1counters), 0, n_units * sizeof(unsigned int), s));
   if (seeds && first_slot < 0 && !state)
     return set_err(ARCHES_E_CONTRACT, "first_slot < 0 needs the stream state (slot source)");
+  if (seeds && with_rng) {  // RNG side products for K3 (run_batch forks them onto a side stream)
+    const int rc = launch_rng(plan, n_streams, n_slots, seeds, first_slot, state, ws, s);
+    if (rc) return rc;
+  }
   K1Out o{ws_at<double>(ws, w.sigma2), nullptr, ws_at<float2>(ws, w.coef),
           ws_at<double>(ws, w.k1parts), ws_at<unsigned int>(ws, w.k1counters),
-          K1_NOISE | K1_MMSE | K1_AI, seeds ? ws_at<double>(ws, w.rng) : nullptr, seeds,
+          K1_NOISE | K1_MMSE | K1_AI, nullptr, seeds,
           reinterpret_cast<const unsigned char*>(state),
           state_stride_bytes(plan->dev.window_length, plan->dev.dapp_window), first_slot, n_slots};
   int rc = plan->k1t_nb ? launch_k1t(plan, n_units, src, o, w, ws, s)
@@ -836,12 +866,31 @@ extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int3
                                 void* h_mmse, void* h_ai, arches_telemetry* tel, arches_kpm* kpm,
                                 arches_message* msg_log, int32_t* msg_count, int32_t msg_cap,
                                 void* ws, arches_stream_t stream) {
-  int rc = arches_ls_analyze(plan, n_streams, n_slots, y, pilots, seeds, first_slot, state,
-                             nullptr, ws, stream);
+  if (!plan || !seeds) return set_err(ARCHES_E_CONTRACT, "bad run_batch args");
+  if (first_slot < 0 && !state)
+    return set_err(ARCHES_E_CONTRACT, "first_slot < 0 needs the stream state (slot source)");
+  // fork: the RNG side products (independent of the grid) on a side stream
+  // next to K1; join before K2 / K3 consume them (a fork-join node pair when
+  // the caller captures this into a CUDA graph)
+  static thread_local cudaStream_t side = nullptr;
+  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (!side) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaEventRecord(ev_fork, s));
+  CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
+  int rc = launch_rng(plan, n_streams, n_slots, seeds, first_slot, state, ws, side);
   if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(ev_join, side));
+  rc = ls_analyze_impl(plan, n_streams, n_slots, y, pilots, seeds, first_slot, state, nullptr, ws,
+                       stream, false);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
   rc = experts_equalize_impl(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
-                             state, h_mmse, h_ai, tel, ws, stream,
-                             /* RNG side products from K1 */ true);
+                             state, h_mmse, h_ai, tel, ws, stream, /* RNG side products */ true);
   if (rc) return rc;
   return arches_kpm_scan(plan, n_streams, n_slots, tel, regime, tree, state, kpm, msg_log,
                          msg_count, msg_cap, stream);

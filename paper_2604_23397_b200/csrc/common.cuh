@@ -187,6 +187,10 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 // (CTA, unit) segment, at the segment's first tile.  K3 adds the segments.
 __host__ __device__ inline bool k2_segment_start(int item, int n_tiles, int n_items, int G) {
   if (item % n_tiles == 0) return true;
+  if ((long long)n_items * G < 0x7fffffffLL) {  // 32-bit division is enough (and much cheaper)
+    const unsigned b = ((unsigned)item * (unsigned)G + (unsigned)n_items - 1u) / (unsigned)n_items;
+    return b < (unsigned)G && (b * (unsigned)n_items) / (unsigned)G == (unsigned)item;
+  }
   const long long b = ((long long)item * G + n_items - 1) / n_items;  // ceil
   return b < G && (b * n_items) / G == item;
 }

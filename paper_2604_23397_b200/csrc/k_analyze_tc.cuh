@@ -51,6 +51,26 @@ struct K1TArgs {
   int n_chunks, nb;        // chunks per row, MMA N
   long long* dbg;          // profiling aid: per-CTA wait cycles [G][8] (null = off)
 };
+
+// RNG side products of each unit (Philox CRC uniform of rng.stream(seed, "crc",
+// slot), LCID4 split of _lcid4_jitter(slot); rng.py:24-34, phy_pipeline.py:
+// 217-222,347-350): one thread per unit.  Independent of the grid, so
+// arches_run_batch runs it on a forked stream next to K1.
+__global__ void k_rng_units(const PlanDev P, double* rng, const uint64_t* seeds,
+                            const unsigned char* state, size_t state_stride, long long first_slot,
+                            int n_slots, int n_units) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int stream = u / n_slots;
+  const long long base = first_slot >= 0
+      ? first_slot
+      : (long long)*reinterpret_cast<const int64_t*>(state + (size_t)stream * state_stride);
+  const long long slot = base + (u - stream * n_slots);
+  rng[2 * u] = arches_rng::stream_first_uniform(seeds[stream], P.crc_key, (uint64_t)slot);
+  const double jit = arches_rng::lcid4_jitter((uint64_t)slot);
+  const double f = __dadd_rn(P.lcid4_fraction, __dmul_rn(P.lcid4_jitter, jit));
+  rng[2 * u + 1] = fmin(fmax(f, 0.0), 1.0);
+}
 #define K1T_T0() long long t0_ = a.dbg ? clock64() : 0
 #define K1T_T1(slot) if (a.dbg) atomicAdd((unsigned long long*)&a.dbg[blockIdx.x * 8 + (slot)], (unsigned long long)(clock64() - t0_))
 
@@ -87,7 +107,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
     k1_tc(const PlanDev P, const K1TArgs a, const int n_items,
           const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
           const __grid_constant__ CUtensorMap tm2, const __grid_constant__ CUtensorMap tm3) {
-  extern __shared__ __align__(1024) unsigned char sm[];
+  extern __shared__ __align__(1024) unsigned char sm1k[];
   __shared__ __align__(8) uint64_t s_full[K1T_STAGES], s_empty[K1T_STAGES];
   __shared__ __align__(8) uint64_t s_conv[K1T_MBUF], s_mfree[K1T_MBUF], s_w;
   __shared__ __align__(8) uint64_t s_accf[K1T_ACC], s_acce[K1T_ACC];
@@ -98,13 +118,13 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
   const int NT = 32 * K1T_CONV_WARPS;
   const int G = gridDim.x;
   const int cpp = a.cpp;
-  unsigned char* raw = sm;                                            // [STAGES][2 atoms]
-  unsigned char* mbuf = sm + (size_t)K1T_STAGES * K1T_RAW_BYTES;      // [MBUF][hi | lo]
+  unsigned char* raw = sm1k;                                            // [STAGES][2 atoms]
+  unsigned char* mbuf = sm1k + (size_t)K1T_STAGES * K1T_RAW_BYTES;      // [MBUF][hi | lo]
   unsigned char* wbuf = mbuf + (size_t)K1T_MBUF * 2 * K1T_OP_BYTES;   // [hi | lo]
   float2* rotsm = reinterpret_cast<float2*>(wbuf + 2 * w_bytes);      // [n_chunks][L] chunk phases
 
   if (threadIdx.x == 0) {
-    if (smem_u32(sm) & 1023u) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
+    if (smem_u32(sm1k) & 1023u) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
     for (int s = 0; s < K1T_STAGES; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&s_empty[s], NT);
@@ -351,8 +371,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
 
 // One CTA per unit: thread o sums output o (= (a, d, component)) over the parts
 // in part order (fp64, loads in flight together); warp 0 forms sigma2
-// (Parseval), then the MMSE and AI taps; the last warp draws the unit's RNG side
-// products (Philox CRC uniform, LCID4 split) in parallel.
+// (Parseval), then the MMSE and AI taps.
 #define K1T_FIN_THREADS 512
 __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev P, const K1TArgs a,
                                                                  int n_units, K1Out o) {
@@ -361,21 +380,7 @@ __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev 
   __shared__ double s_sg;
   const int u = blockIdx.x;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int stream = u / o.n_slots;
   const int L = P.L, ncol = 2 * L, AD = P.A * P.D, nout = AD * ncol;
-  if (w == K1T_FIN_THREADS / 32 - 1 && lane < 2 && o.rng) {
-    const long long base = o.first_slot >= 0
-        ? o.first_slot
-        : (long long)*reinterpret_cast<const int64_t*>(o.state + (size_t)stream * o.state_stride);
-    const long long slot = base + (u - stream * o.n_slots);
-    if (lane == 0) {
-      o.rng[2 * u] = arches_rng::stream_first_uniform(o.seeds[stream], P.crc_key, (uint64_t)slot);
-    } else {
-      const double jit = arches_rng::lcid4_jitter((uint64_t)slot);
-      const double f = __dadd_rn(P.lcid4_fraction, __dmul_rn(P.lcid4_jitter, jit));
-      o.rng[2 * u + 1] = fmin(fmax(f, 0.0), 1.0);
-    }
-  }
   double* acc = nout <= 4096 ? s_bins : o.parts + (size_t)u * (2 * (size_t)AD * L + 2);
   const int np = a.parts;
   const size_t pstride = (size_t)P.D * a.n_g * 128 * ncol;  // next part, same (d, g, row)
