@@ -469,7 +469,8 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
       const int R = 2 * na * d.D, ncol = ((2 * R + 15) / 16) * 16, ng = ncol / 8;
       const int n_b = (ncol / 2) * 4 * d.tc_kb;  // B entries: <= 2 per thread of 512
       const int as = grp ? 4 : d.A;               // antennas per stage
-      sm = 2 * (size_t)(as + 1) * d.T * ARCHES_TILE * sizeof(float2) + 4 * (size_t)d.tc_kb * ng * 256;
+      const int nbuf = grp ? 2 : 3;  // B operands in flight (k2_tc NBUF)
+      sm = 2 * (size_t)(as + 1) * d.T * ARCHES_TILE * sizeof(float2) + 2 * nbuf * (size_t)d.tc_kb * ng * 256;
       if (grp) sm += (size_t)21 * TC_THREADS * sizeof(float);  // MRC sums across groups
       if (sm > 227 * 1024 || n_b > 2 * TC_THREADS || ncol > 64) sm = 0;
     }
@@ -752,7 +753,7 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
   {                                                                                          \
     auto kern = tmap ? k2_tc<NA_, ND_, STD_, true, GRP_> : k2_tc<NA_, ND_, STD_, false, GRP_>; \
     CUDA_TRY(ensure_smem(kern, smem));                                                       \
-    kern<<<grid, TC_THREADS, smem, s>>>(d, a, n_items, tm_y, tm_x);                          \
+    kern<<<grid, TC_BLOCK, smem, s>>>(d, a, n_items, tm_y, tm_x);                            \
     LAUNCH_CHECK();                                                                          \
     /* K3 locates the (CTA, unit) segments in tile units */                                  \
     k3_finalize<<<(n_units * 32 + K3_THREADS - 1) / K3_THREADS, K3_THREADS, 0, s>>>(         \

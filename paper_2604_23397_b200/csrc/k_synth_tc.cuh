@@ -22,7 +22,8 @@
 #include "common.cuh"
 #include "k_synth_eq.cuh"
 
-#define TC_THREADS 512
+#define TC_THREADS 512                   // epilogue threads: 128 subcarriers x 2 experts x 2 symbol halves
+#define TC_BLOCK (TC_THREADS + 32)       // + the producer / MMA warp
 
 __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   // SWIZZLE_NONE K-major canonical layout: core matrices of 8 rows x 16 B,
@@ -279,16 +280,22 @@ __device__ __forceinline__ void eq_grp_half(const float2 (&h)[NA][ND], const flo
 }
 
 template <int NA, int ND, bool kStd, bool kTmap, bool kGrp = false>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TC_BLOCK, 1)
     k2_tc(const PlanDev P, const K2Args args, const int n_items,
           const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ CUtensorMap tm_x) {
   constexpr int R = 2 * NA * ND;                    // complex outputs: AI then MMSE
   constexpr int NCOL = ((2 * R + 15) / 16) * 16;    // MMA N (real columns)
   constexpr int NG = NCOL / 8;
   constexpr int CPE = 2 * NA * ND;                  // D columns per expert
+  // B operands / TMEM accumulators in flight: item i's MMA is issued as soon as
+  // the epilogue of item i - LEAD is done, so its latency hides behind a whole
+  // epilogue (massive-MIMO plans keep one item of lead: shared memory)
+  constexpr int LEAD = kGrp ? 1 : 2;
+  constexpr int NBUF = LEAD + 1;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t s_full[2];       // stage landed
-  __shared__ __align__(8) uint64_t s_mma[2];        // accumulator ready
+  __shared__ __align__(8) uint64_t s_mma[NBUF];     // accumulator ready
+  __shared__ __align__(8) uint64_t s_bready[NBUF];  // B(i) written (512 arrivals)
   __shared__ uint32_t s_tmem;
   __shared__ double s_red[2][11][8];
   const int KB = P.tc_kb, L4 = 4 * KB;
@@ -313,8 +320,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const size_t stage_elems = (size_t)(AS + 1) * T * ARCHES_TILE;
   const size_t coef_stride = coef_floats2(P);
   float2* sYX = reinterpret_cast<float2*>(sm);                               // [2][stage]
-  unsigned char* sB = sm + 2 * stage_elems * sizeof(float2);                 // [2][hi | lo]
-  float* gacc = reinterpret_cast<float*>(sB + 4 * (size_t)KB * NG * 256) + threadIdx.x;  // [21][512] (kGrp)
+  unsigned char* sB = sm + 2 * stage_elems * sizeof(float2);                 // [NBUF][hi | lo]
+  float* gacc = reinterpret_cast<float*>(sB + 2 * NBUF * (size_t)KB * NG * 256) + threadIdx.x;  // [21][512] (kGrp)
   const int n_all = (NCOL / 2) * L4;                                         // B entries
   const uint32_t ACC0 = 128;                                                 // TMEM columns
   // this thread's <= 2 B entries (output column pair r, tap l): source offsets
@@ -344,14 +351,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 
   if (threadIdx.x == 0) {
-    const uint32_t arrivals = kTmap ? 1u : (uint32_t)(TC_THREADS / 32);
-    mbar_init(&s_full[0], arrivals);
-    mbar_init(&s_full[1], arrivals);
-    mbar_init(&s_mma[0], 1);
-    mbar_init(&s_mma[1], 1);
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(&s_mma[b], 1);
+      mbar_init(&s_bready[b], TC_THREADS);
+    }
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -361,12 +369,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = s_tmem;
   const uint32_t lane_base = tmem + ((uint32_t)(q4 * 32) << 16);
 
-  auto issue_tma = [&](int u, int tile, int gr, int stage) {
+  auto issue_tma = [&](int u, int tile, int gr, int stage) {  // producer warp (all lanes)
     const uint64_t pol = l2_evict_first_policy();
     float2* dst = sYX + (size_t)stage * stage_elems;
     const bool with_x = gr == ngrp - 1;  // tx rows: needed by the last group only
-    if constexpr (kTmap) {  // thread 0: two tensor copies (y rows of the group, tx rows)
-      if (threadIdx.x == 0) {
+    if constexpr (kTmap) {  // lane 0: two tensor copies (y rows of the group, tx rows)
+      if (lane == 0) {
         const size_t ybytes = (size_t)AS * T * ARCHES_TILE * sizeof(float2);
         mbar_arrive_expect_tx(&s_full[stage], (uint32_t)(with_x ? stage_elems * sizeof(float2) : ybytes));
         tma_load_3d(dst, &tm_y, tile * 2 * ARCHES_TILE, gr * AS * T, u, &s_full[stage], pol);
@@ -374,14 +382,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tma_load_3d(dst + (size_t)AS * T * ARCHES_TILE, &tm_x, tile * 2 * ARCHES_TILE, 0, u,
                       &s_full[stage], pol);
       }
-    } else if (lane == 0) {  // lane 0 of every warp: rows r = warp (mod 16)
+    } else {  // one 1-D bulk copy per row, rows spread over the lanes
       const int k0 = tile * ARCHES_TILE;
       const uint32_t rowb = (uint32_t)min(ARCHES_TILE, P.N - k0) * sizeof(float2);
       const int rows = AS * T + (with_x ? T : 0);
-      const int nw = TC_THREADS / 32;
-      const int mine = (rows - warp + nw - 1) / nw;
-      mbar_arrive_expect_tx(&s_full[stage], rowb * (uint32_t)mine);
-      for (int r = warp; r < rows; r += nw) {
+      if (lane == 0) mbar_arrive_expect_tx(&s_full[stage], rowb * (uint32_t)rows);
+      __syncwarp();
+      for (int r = lane; r < rows; r += 32) {
         const float2* src = (r < AS * T) ? args.y + ((size_t)u * P.A * T + (size_t)gr * AS * T + r) * P.N + k0
                                          : args.tx + ((size_t)u * T + (r - AS * T)) * P.N + k0;
         bulk_g2s(dst + (size_t)r * ARCHES_TILE, src, rowb, &s_full[stage], pol);
@@ -413,7 +420,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   };
-  auto issue_mma = [&](int buf) {  // thread 0 only, after a CTA barrier
+  auto issue_mma = [&](int buf) {  // producer warp lane 0, once B(buf) is written
     tc_fence_after();
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NCOL >> 3) << 17) |
                            ((uint32_t)(ARCHES_TILE >> 4) << 24);
@@ -430,10 +437,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     umma_commit(&s_mma[buf]);
   };
 
+  // next work item after (u, tile, gr)
+  auto advance = [&](int& au, int& at, int& ag) {
+    if (++ag == ngrp) {
+      ag = 0;
+      if (++at == n_tiles) {
+        at = 0;
+        ++au;
+      }
+    }
+  };
   int u = (lo / ngrp) / n_tiles, tile = (lo / ngrp) - u * n_tiles, gr = 0;
-  // ---- prologue: A operand (twiddle rows) -> TMEM, item 0 data + B(0) + MMA(0)
+  const int count = hi - lo;
+  // ---- prologue: A operand (twiddle rows) -> TMEM
   if (lo < hi) {
-    issue_tma(u, tile, 0, 0);
     if (warp < 4) {
       const float4* arow = reinterpret_cast<const float4*>(P.tc_a) + (size_t)j * (KB * 4);
       for (int c = 0; c < KB; ++c) {
@@ -458,21 +475,56 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
-    float2 cv[2];
-    load_b(u, tile, 0, cv);
-    write_b(0, cv);
-    tc_fence_before();
-    __syncthreads();
-    if (threadIdx.x == 0) issue_mma(0);
   }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == TC_THREADS / 32) {
+    // ---------------- producer / MMA warp.  B(j) written means the epilogue of
+    // item j - LEAD is finished: MMA(j) goes out (its accumulator was read by
+    // item j - NBUF), and the stage item j - LEAD used is refilled with item
+    // j - LEAD + 2.  The epilogue warps never meet at a CTA barrier for this.
+    int tu = u, tt = tile, tg = gr;  // next item to load
+    for (int k = 0; k < 2 && k < count; ++k) {
+      issue_tma(tu, tt, tg, k);
+      advance(tu, tt, tg);
+    }
+    for (int jj = 0; jj < count; ++jj) {
+      mbar_wait(&s_bready[jj % NBUF], (jj / NBUF) & 1);
+      if (lane == 0) issue_mma(jj % NBUF);
+      __syncwarp();
+      const int nx = jj - LEAD + 2;
+      if (nx >= 2 && nx < count) {
+        issue_tma(tu, tt, tg, nx & 1);
+        advance(tu, tt, tg);
+      }
+    }
+  } else {
+  if (lo < hi) {  // B of the first LEAD items
+    int bu = u, bt = tile, bg = gr;
+    for (int k = 0; k < LEAD && k < count; ++k) {
+      float2 cv[2];
+      load_b(bu, bt, bg, cv);
+      write_b(k, cv);
+      tc_fence_before();
+      mbar_arrive(&s_bready[k]);
+      advance(bu, bt, bg);
+    }
+  }
+  // the item LEAD ahead of the current one (its B operand is written this iteration)
+  int lu = u, lt = tile, lg = gr;
+  for (int k = 0; k < LEAD; ++k) advance(lu, lt, lg);
 
   // per-thread telemetry sums, kept across the tiles of one unit
   float sa = 0.f, sp = 0.f, sre = 0.f, sim = 0.f, syy = 0.f, sxx = 0.f;
   int seg_t0 = tile;  // first tile of the current (CTA, unit) segment
   float nv = lo < hi ? (float)__ldg(&args.nv[u]) : 0.f;
   for (int item = lo, i = 0; item < hi; ++item, ++i) {
-    const int buf = i & 1, ph = (i >> 1) & 1;
+    const int buf = i & 1, ph = (i >> 1) & 1;       // y / tx stage
+    const int mb = i % NBUF, mph = (i / NBUF) & 1;  // B operand + TMEM accumulator
     const bool has_next = item + 1 < hi;
+    const bool has_lead = item + LEAD < hi;
     const bool last_grp = gr + 1 == ngrp;
     const bool last_tile = tile + 1 == n_tiles && last_grp;  // last item of the unit
     const int gn = last_grp ? 0 : gr + 1;
@@ -484,10 +536,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool valid = kk < P.N;
     // ---- next item's data + coefficients in flight during this item's work
     float2 cv[2];
-    if (has_next) {
-      issue_tma(un, tn, gn, buf ^ 1);
-      load_b(un, tn, gn, cv);
-    }
+    if (has_lead) load_b(lu, lt, lg, cv);
     if constexpr (kTmap) {
       // L2 prefetch pf_dist items ahead: the shared-memory stages hold one item
       // in flight, the L2 holds the next ones (tensor-map prefetch, one
@@ -504,10 +553,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     // ---- this expert's synthesised taps
-    mbar_wait(&s_mma[buf], ph);
+    mbar_wait(&s_mma[mb], mph);
     tc_fence_after();
     float vals[CPE];
-    tmem_ld_n<CPE>(lane_base + ACC0 + 64u * buf + (uint32_t)(ex * CPE), vals);
+    tmem_ld_n<CPE>(lane_base + ACC0 + 64u * mb + (uint32_t)(ex * CPE), vals);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     float2 h[NA][ND];
 #pragma unroll
@@ -598,12 +647,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         s_red[buf][9 + ex][col] = r4;
       }
       sa = sp = sre = sim = syy = sxx = 0.f;
+      named_bar(1, TC_THREADS);  // every warp's partials in s_red[buf]
     }
-    // ---- B(i+1) -> shared memory, one barrier, MMA(i+1)
-    if (has_next) write_b(buf ^ 1, cv);
-    tc_fence_before();
-    __syncthreads();
-    if (has_next && threadIdx.x == 0) issue_mma(buf ^ 1);
+    // ---- B(i + LEAD) -> shared memory; signals the producer / MMA warp
+    if (has_lead) {
+      write_b((i + LEAD) % NBUF, cv);
+      tc_fence_before();
+      mbar_arrive(&s_bready[(i + LEAD) % NBUF]);
+    }
     // ---- segment partial (fixed order); per-unit finalisation runs in K3
     if (flush && warp == 1 && lane < 11) {
       double acc;
@@ -622,12 +673,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     u = un;
     tile = tn;
     gr = gn;
+    advance(lu, lt, lg);
   }
+  }  // epilogue warps
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // K3 -- per-unit finalisation for the tensor-core K2, one warp per unit: lanes
