@@ -303,11 +303,10 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
     // comb pilots, one chunk ahead of the conversion
     float2 qn[K1T_CP];
     auto load_pilots = [&](int c) {
+      const int mlim = (live && c < c1) ? min(K1T_CP, P.M - c * K1T_CP) : 0;
+      const float2* pc = pl + (size_t)c * K1T_CP * P.D;  // this chunk's first comb point
 #pragma unroll
-      for (int k = 0; k < K1T_CP; ++k) {
-        const int m = c * K1T_CP + k;
-        qn[k] = (live && c < c1 && m < P.M) ? __ldg(&pl[(size_t)m * P.D]) : make_float2(0.f, 0.f);
-      }
+      for (int k = 0; k < K1T_CP; ++k) qn[k] = k < mlim ? __ldg(pc + k * P.D) : make_float2(0.f, 0.f);
     };
     load_pilots(c0);
     for (int c = c0; c < c1; ++c, ++j) {
@@ -347,7 +346,8 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
 #pragma unroll
       for (int k = 0; k < K1T_CP / 2; ++k) {
         const float2 h0 = hv[2 * k], h1 = hv[2 * k + 1];
-        const float4 hi = make_float4(tf32_rna(h0.x), tf32_rna(h0.y), tf32_rna(h1.x), tf32_rna(h1.y));
+        const float4 hi = make_float4(tf32_rna_fast(h0.x), tf32_rna_fast(h0.y), tf32_rna_fast(h1.x),
+                                      tf32_rna_fast(h1.y));
         ah[k ^ sw] = hi;
         // lo = h - hi is exact in fp32 (<= 14 significant bits); the MMA reads its
         // top 11, so the dropped tail is < 2^-22 |h| -- no explicit rounding needed

@@ -80,6 +80,11 @@ __device__ __forceinline__ float tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+// the same rounding (nearest, ties away from zero) in two integer ops for finite
+// inputs -- cvt.rna.tf32 is emulated by a longer sequence on sm_100
+__device__ __forceinline__ float tf32_rna_fast(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 
 
 // byte offset of element (row, kappa) of a K-major SWIZZLE_NONE operand with
@@ -411,8 +416,8 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
     for (int q = 0; q < 2; ++q) {
       if (q * TC_THREADS + (int)threadIdx.x >= n_all) break;
       const float2 c = cv[q];
-      const float rh = tf32_rna(c.x), rl = tf32_rna(c.x - rh);
-      const float ih = tf32_rna(c.y), il = tf32_rna(c.y - ih);
+      const float rh = tf32_rna_fast(c.x), rl = tf32_rna_fast(c.x - rh);
+      const float ih = tf32_rna_fast(c.y), il = tf32_rna_fast(c.y - ih);
       *reinterpret_cast<float2*>(bhi + o0[q]) = make_float2(rh, -ih);
       *reinterpret_cast<float2*>(bhi + o1[q]) = make_float2(ih, rh);
       *reinterpret_cast<float2*>(blo + o0[q]) = make_float2(rl, -il);
