@@ -287,7 +287,8 @@ def run_ours(a, rank, world, dist):
     t_ms = e0.elapsed_time(e1)
     t_max = t_ms
     if dist is not None:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_ms], dtype=torch.float64,
+                          device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     value = K * U * world / (t_max / 1000.0)
@@ -355,7 +356,8 @@ def run_ours(a, rank, world, dist):
     barrier()
     te = e2.elapsed_time(e3)
     if dist is not None:
-        tt = torch.tensor([te], dtype=torch.float64, device=dev)
+        tt = torch.tensor([te], dtype=torch.float64,
+                          device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         te = float(tt.item())
     recs = kpm_h.numpy().view(_lib.KPM_DTYPE)
@@ -440,8 +442,14 @@ def main():
     if world > 1:
         import torch.distributed as dist_mod
         local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one process per GPU; ARCHES_DIST_BACKEND=gloo is a test hook that lets
+        # several ranks share one GPU (the timing reduction then goes via the host)
+        backend = os.environ.get("ARCHES_DIST_BACKEND", "nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        if backend == "nccl":
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist_mod.init_process_group(backend)
         dist = dist_mod
     run_ours(a, rank, world, dist)
     if dist is not None:

@@ -211,7 +211,7 @@ int arches_kpm_scan(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                     int32_t* msg_count, int32_t msg_cap, arches_stream_t stream);
 
 /* Same contract and results as arches_kpm_scan, one thread walking every slot
- * of a stream (the literal restatement; the default scan is warp-parallel).
+ * of a stream (the literal restatement; the default scan is block-parallel).
  * Kept exported so parity tests can cross-check the two forms. */
 int arches_kpm_scan_sequential(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                                const arches_telemetry* tel, const int8_t* regime,
@@ -219,8 +219,12 @@ int arches_kpm_scan_sequential(const arches_plan* plan, int32_t n_streams, int32
                                arches_message* msg_log, int32_t* msg_count, int32_t msg_cap,
                                arches_stream_t stream);
 
-/* K1 + K2 + K4 for one batch (the per-step hot path); first_slot < 0 takes the
- * slot numbering from the device state (CUDA-graph friendly). */
+/* The per-step hot path for one batch: RNG side products || K1 (+ finalize) ->
+ * K2 -> K3 -> K4; first_slot < 0 takes the slot numbering from the device state
+ * (CUDA-graph friendly).  The RNG kernel runs on an internal stream forked from
+ * and joined back into `stream` (event fork/join, so it captures into a graph);
+ * when the call returns, all work is ordered on `stream` as for the other
+ * entry points.  seeds is required. */
 int arches_run_batch(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                      int64_t first_slot, const void* y, const void* tx, const void* pilots,
                      const double* noise_var, const uint64_t* seeds, const int8_t* regime,
