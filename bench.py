@@ -423,7 +423,7 @@ def run_ours(a, rank, world, dist):
             "e2e": {"value": K * U * world / (te / 1000.0), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "latency": lat,
-            "gpu_launches": 5 * K,  # K1 + K1 finalize + K2 + K3 + K4 per step (one CUDA graph)
+            "gpu_launches": 6 * K,  # RNG, K1, K1 finalize, K2, K3, K4 per step (one CUDA graph)
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

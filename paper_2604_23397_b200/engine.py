@@ -3,7 +3,7 @@
 `ArchesPlan` wraps `arches_plan` (geometry + PipelineConfig + MMSE prior +
 control-plane configuration).  `SlotEngine` owns every device buffer for a
 batch of `n_streams` single-layer streams x `n_slots` consecutive slots and
-runs K1 -> K2 -> K4 (`arches_run_batch`) on the current torch CUDA stream,
+runs RNG || K1 -> K1 finalize -> K2 -> K3 -> K4 (`arches_run_batch`) on the current torch CUDA stream,
 optionally through a captured CUDA graph.  Control state (mode, windows,
 pending messages, dApp window, fail-safe) stays device-resident across
 batches, so consecutive `run()` calls continue each stream's slot sequence
@@ -222,7 +222,7 @@ class SlotEngine:
         self.next_slot += self.S
 
     def capture_graph(self):
-        """Capture K1 -> K2 -> K4 once; later run() calls replay it."""
+        """Capture one step (RNG || K1 -> K1 finalize -> K2 -> K3 -> K4) once; later run() calls replay it."""
         import torch
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
@@ -234,7 +234,7 @@ class SlotEngine:
         self.graph = g
 
     def launches_per_run(self) -> int:
-        return 3  # K1, K2, K4 (+ one memset node)
+        return 6  # RNG (forked stream), K1, K1 finalize, K2, K3, K4 (tensor-core plans)
 
     def switch_copy(self):
         """K5: reference aliasing semantics -- copy MMSE into the AI buffer for mode-1 units."""
