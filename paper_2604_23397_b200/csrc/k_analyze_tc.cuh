@@ -377,14 +377,14 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
 __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev P, const K1TArgs a,
                                                                  int n_units, K1Out o) {
   __shared__ double s_bins[4096];
-  __shared__ double s_e[32];
-  __shared__ double s_sg;
+  __shared__ double s_e[K1T_FIN_THREADS / 32], s_g[K1T_FIN_THREADS / 32];
   const int u = blockIdx.x;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int L = P.L, ncol = 2 * L, AD = P.A * P.D, nout = AD * ncol;
   double* acc = nout <= 4096 ? s_bins : o.parts + (size_t)u * (2 * (size_t)AD * L + 2);
   const int np = a.parts;
   const size_t pstride = (size_t)P.D * a.n_g * 128 * ncol;  // next part, same (d, g, row)
+  double sg = 0.0;  // this thread's share of sum_{a,d,l<guard} |B_l|^2
   for (int o2 = tid; o2 < nout; o2 += K1T_FIN_THREADS) {
     const int ad = o2 / ncol, cc = o2 - ad * ncol;
     const int aa = ad / P.D, d = ad - aa * P.D;
@@ -399,36 +399,31 @@ __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev 
       for (int k = 0; k < 8; ++k) sum += v[k];
     }
     acc[o2] = sum;
+    if (cc < 2 * P.guard) sg += sum * sum;
   }
-  {
-    double e = 0.0;
-    for (int o2 = tid; o2 < AD; o2 += K1T_FIN_THREADS) {
-      const int aa = o2 / P.D, d = o2 - aa * P.D;
-      const int row = u * P.A + aa, g = row / 128, r = row - g * 128;
-      for (int q = 0; q < np; ++q) e += __ldcg(a.epart + (size_t)((q * P.D + d) * a.n_g + g) * 128 + r);
-    }
-    e = warp_sum(e);
-    if (lane == 0) s_e[w] = e;
+  double e = 0.0;
+  for (int o2 = tid; o2 < AD; o2 += K1T_FIN_THREADS) {
+    const int aa = o2 / P.D, d = o2 - aa * P.D;
+    const int row = u * P.A + aa, g = row / 128, r = row - g * 128;
+    for (int q = 0; q < np; ++q) e += __ldcg(a.epart + (size_t)((q * P.D + d) * a.n_g + g) * 128 + r);
   }
-  __syncthreads();
-  if (w == 0) {
-    double sg = 0.0;
-    for (int o2 = lane; o2 < AD * P.guard; o2 += 32) {
-      const int ad = o2 / P.guard, l = o2 - ad * P.guard;
-      const double bx = acc[ad * ncol + 2 * l], by = acc[ad * ncol + 2 * l + 1];
-      sg += bx * bx + by * by;
-    }
-    sg = warp_sum(sg);
-    double e = lane < K1T_FIN_THREADS / 32 ? s_e[lane] : 0.0;
-    e = warp_sum(e);
-    const int M = P.M;
-    const double nvhat = (e - sg / (double)M) / ((double)AD * (M - P.guard));
-    if (lane == 0) {
-      o.sigma2[u] = nvhat;
-      s_sg = nvhat + P.ridge;
-    }
+  e = warp_sum(e);
+  sg = warp_sum(sg);
+  if (lane == 0) {
+    s_e[w] = e;
+    s_g[w] = sg;
   }
   __syncthreads();
+  // sigma2 (Parseval): every thread sums the warp partials in the same order
+  double et = 0.0, gt = 0.0;
+#pragma unroll
+  for (int k = 0; k < K1T_FIN_THREADS / 32; ++k) {
+    et += s_e[k];
+    gt += s_g[k];
+  }
+  const double nvhat = (et - gt / (double)P.M) / ((double)AD * (P.M - P.guard));
+  if (tid == 0) o.sigma2[u] = nvhat;
+  const double s_sg = nvhat + P.ridge;
   const double sgm = s_sg;
   const int M = P.M;
   float2* cm = o.coef + (size_t)u * coef_floats2(P);
