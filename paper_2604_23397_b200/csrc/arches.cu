@@ -875,21 +875,33 @@ extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int3
   // the caller captures this into a CUDA graph)
   static thread_local cudaStream_t side = nullptr;
   static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (!side) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  CUDA_TRY(cudaEventRecord(ev_fork, s));
-  CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
-  int rc = launch_rng(plan, n_streams, n_slots, seeds, first_slot, state, ws, side);
-  if (rc) return rc;
-  CUDA_TRY(cudaEventRecord(ev_join, side));
+  if (!side) {
+    // streams / events cannot be created while `stream` is being captured: the
+    // first call made inside a capture runs the RNG in line instead
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+    if (cap == cudaStreamCaptureStatusNone) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+  }
+  int rc;
+  if (side) {
+    CUDA_TRY(cudaEventRecord(ev_fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
+    rc = launch_rng(plan, n_streams, n_slots, seeds, first_slot, state, ws, side);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(ev_join, side));
+  } else {
+    rc = launch_rng(plan, n_streams, n_slots, seeds, first_slot, state, ws, s);
+    if (rc) return rc;
+  }
   rc = ls_analyze_impl(plan, n_streams, n_slots, y, pilots, seeds, first_slot, state, nullptr, ws,
                        stream, false);
   if (rc) return rc;
-  CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
+  if (side) CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
   rc = experts_equalize_impl(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
                              state, h_mmse, h_ai, tel, ws, stream, /* RNG side products */ true);
   if (rc) return rc;

@@ -146,3 +146,52 @@ def test_closed_loop_matches_reference(lid, batches):
     trig = {0: "policy", 1: "failsafe", 2: "oracle", 3: "fixed"}
     assert [[int(x["mode"]), int(x["decided_at_ns"]), int(x["deliverable_at_ns"]),
              trig[int(x["trigger"])]] for x in msgs] == m["messages"]
+
+
+def test_graph_captured_on_a_fresh_thread_matches_eager():
+    """First arches_run_batch call of a host thread made inside a CUDA-graph
+    capture (no side stream can be created then: the RNG kernel runs in line)
+    gives the same records as eager runs."""
+    import threading
+
+    import torch
+    geo = SlotGeometry(n_ant=4, n_prb=12)
+    scens = default_scenarios(21, geo)
+    cs = CellScene(geo, scens, "good")
+    regimes = ["good", "poor"] * 4
+    slots = [cs.next_slot(r) for r in regimes]
+    inputs = dict(y=np.stack([to_device_layout(s.y) for s in slots]),
+                  tx=np.stack([s.tx.T for s in slots]).astype(np.complex64),
+                  noise_var=[s.noise_var for s in slots],
+                  regime=[1 if r == "good" else 0 for r in regimes])
+
+    def make():
+        eng = _engine(geo, 1.25, PipelineConfig(), n_slots=len(slots), policy="oracle")
+        eng.set_streams(cs.pilots[None], [21])
+        eng.load(**inputs)
+        return eng
+
+    ref = make()
+    ref.run()
+    ref.run()
+    want = ref.kpm_records().copy()
+    got, err = {}, []
+
+    def worker():
+        try:
+            torch.cuda.set_device(0)
+            eng = make()
+            eng.capture_graph()  # the thread's first run_batch call happens inside the capture
+            eng.run()
+            eng.run()
+            torch.cuda.synchronize()
+            got["kpm"] = eng.kpm_records().copy()
+        except Exception as e:  # surfaced below
+            err.append(e)
+
+    t = threading.Thread(target=worker)
+    t.start()
+    t.join()
+    assert not err, err
+    for f in want.dtype.names:
+        assert np.array_equal(got["kpm"][f], want[f]), f
