@@ -79,7 +79,7 @@ def main(rep):
         print("opcode mix: " + ", ".join(f"{k} {v / tot * 100:.1f}%" for k, v in op.most_common(10)))
         s = sum(st.values()) or 1.0
         print("\nstall reasons: " + ", ".join(f"{k[6:]} {v / s * 100:.1f}%" for k, v in st.most_common(6)))
-        tc = [k for k in op if k.startswith("UTC") or k in ("LDTM", "STTM", "UBLKCP")]
+        tc = [k for k in op if k.startswith(("UTC", "UTMA", "UBLK")) or k in ("LDTM", "STTM")]
         if tc:
             print("\nBlackwell-native instructions executed: " + ", ".join(f"{k} x{int(op[k])}" for k in sorted(tc)))
 
