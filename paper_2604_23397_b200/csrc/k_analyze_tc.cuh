@@ -338,7 +338,9 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
         const float4 v = src[(k >> 3) * (K1T_ATOM / 16) + ((k & 7) ^ sw)];
         const float2 p = qv[k];
         const float n2 = p.x * p.x + p.y * p.y;
-        const float inv = n2 > 0.f ? 1.0f / n2 : 0.f;
+        float inv;  // 1/|p|^2 within 1 ulp (exact for the unit-modulus QPSK pilots); 0 for padding
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(n2));
+        inv = n2 > 0.f ? inv : 0.f;
         hv[k] = make_float2((p.x * v.x + p.y * v.y) * inv, (p.x * v.y - p.y * v.x) * inv);
         e32 = fmaf(hv[k].x, hv[k].x, fmaf(hv[k].y, hv[k].y, e32));
       }
