@@ -290,6 +290,12 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
 
   // ---------------- converter warps: thread = row
   const int t = threadIdx.x;
+  const int pD = P.D;
+  // this row's SWIZZLE_128B positions of the 8 16-byte groups (byte offsets)
+  const uint32_t sw = (uint32_t)(t & 7);
+  uint32_t swz[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) swz[k] = ((uint32_t)k ^ sw) * 16u;
   int j = 0;
   const long long t_start = clock64();
   for (int item = blockIdx.x; item < n_items; item += G) {
@@ -304,9 +310,12 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
     float2 qn[K1T_CP];
     auto load_pilots = [&](int c) {
       const int mlim = (live && c < c1) ? min(K1T_CP, P.M - c * K1T_CP) : 0;
-      const float2* pc = pl + (size_t)c * K1T_CP * P.D;  // this chunk's first comb point
+      const float2* pc = pl + (size_t)c * K1T_CP * pD;  // this chunk's first comb point
 #pragma unroll
-      for (int k = 0; k < K1T_CP; ++k) qn[k] = k < mlim ? __ldg(pc + k * P.D) : make_float2(0.f, 0.f);
+      for (int k = 0; k < K1T_CP; ++k) {
+        qn[k] = k < mlim ? __ldg(pc) : make_float2(0.f, 0.f);
+        pc += pD;
+      }
     };
     load_pilots(c0);
     for (int c = c0; c < c1; ++c, ++j) {
@@ -327,15 +336,14 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
       }
       // row t, 16-byte group k of atom a at a*16K + t*128 + (k ^ (t & 7))*16
       // (SWIZZLE_128B); group = (y[2m].re, .im, y[2m+1].re, .im), m = 16c + 8a + k
-      const float4* src = reinterpret_cast<const float4*>(raw + (size_t)s * K1T_RAW_BYTES) + t * 8;
-      float4* ah = reinterpret_cast<float4*>(mbuf + (size_t)b * 2 * K1T_OP_BYTES) + t * 8;
-      float4* al = reinterpret_cast<float4*>(mbuf + (size_t)b * 2 * K1T_OP_BYTES + K1T_OP_BYTES) + t * 8;
-      const int sw = t & 7;
+      const unsigned char* src = raw + (size_t)s * K1T_RAW_BYTES + t * 128;
+      unsigned char* ah = mbuf + (size_t)b * 2 * K1T_OP_BYTES + t * 128;
+      unsigned char* al = ah + K1T_OP_BYTES;
       float2 hv[K1T_CP];
       float e32 = 0.f;
 #pragma unroll
       for (int k = 0; k < K1T_CP; ++k) {
-        const float4 v = src[(k >> 3) * (K1T_ATOM / 16) + ((k & 7) ^ sw)];
+        const float4 v = *reinterpret_cast<const float4*>(src + (k >> 3) * K1T_ATOM + swz[k & 7]);
         const float2 p = qv[k];
         const float n2 = p.x * p.x + p.y * p.y;
         float inv;  // 1/|p|^2 within 1 ulp (exact for the unit-modulus QPSK pilots); 0 for padding
@@ -350,10 +358,10 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
         const float2 h0 = hv[2 * k], h1 = hv[2 * k + 1];
         const float4 hi = make_float4(tf32_rna_fast(h0.x), tf32_rna_fast(h0.y), tf32_rna_fast(h1.x),
                                       tf32_rna_fast(h1.y));
-        ah[k ^ sw] = hi;
+        *reinterpret_cast<float4*>(ah + swz[k]) = hi;
         // lo = h - hi is exact in fp32 (<= 14 significant bits); the MMA reads its
         // top 11, so the dropped tail is < 2^-22 |h| -- no explicit rounding needed
-        al[k ^ sw] = make_float4(h0.x - hi.x, h0.y - hi.y, h1.x - hi.z, h1.y - hi.w);
+        *reinterpret_cast<float4*>(al + swz[k]) = make_float4(h0.x - hi.x, h0.y - hi.y, h1.x - hi.z, h1.y - hi.w);
       }
       // raw stage consumed: every loaded value has been used above, so the
       // TMA refill cannot race the shared-memory reads
