@@ -232,6 +232,30 @@ int arches_run_batch(const arches_plan* plan, int32_t n_streams, int32_t n_slots
                      arches_telemetry* tel, arches_kpm* kpm, arches_message* msg_log,
                      int32_t* msg_count, int32_t msg_cap, void* ws, arches_stream_t stream);
 
+/* Pipelined form of arches_run_batch for a sequence of batches (the slots of
+ * consecutive steps).  The control tail of the batch -- RNG side products, K3
+ * (per-unit telemetry + KPM candidates) and K4 (KPM scan / decision policy) --
+ * runs on an internal stream of the plan and overlaps the next call's K1; the
+ * heavy kernels (K1, K1 finalize, K2) stay on `stream`.  Results are identical
+ * to arches_run_batch.  Ordering contract:
+ *  - the outputs of the tail (tel, kpm, msg_log, msg_count, state) and the
+ *    inputs it reads (regime, tree, seeds) belong to the library until
+ *    arches_join(plan, stream) -- do not read or overwrite them before;
+ *  - h_mmse / h_ai / y / tx / noise_var follow `stream` order as usual;
+ *  - one thread at a time per plan; arches_run_batch joins a pending tail first;
+ *  - a CUDA-graph capture must contain its arches_join, and the plan's first
+ *    async call must happen outside capture (the internal stream is created then).
+ * Same arguments as arches_run_batch. */
+int arches_run_batch_async(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                           int64_t first_slot, const void* y, const void* tx, const void* pilots,
+                           const double* noise_var, const uint64_t* seeds, const int8_t* regime,
+                           const arches_tree* tree, void* state, void* h_mmse, void* h_ai,
+                           arches_telemetry* tel, arches_kpm* kpm, arches_message* msg_log,
+                           int32_t* msg_count, int32_t msg_cap, void* ws, arches_stream_t stream);
+/* Order `stream` after every pending arches_run_batch_async tail of the plan
+ * (no-op when none is pending). */
+int arches_join(const arches_plan* plan, arches_stream_t stream);
+
 /* ---- K5: zero-gap switch, reference aliasing semantics ---------------
  * switch_select (phy_pipeline.py:81-91): for every unit whose kpm.mode == 1
  * copy the MMSE output into the AI (downstream) buffer; mode 0 is a no-op. */

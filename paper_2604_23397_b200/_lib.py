@@ -81,6 +81,9 @@ _SIGS = {
                                              C.c_int32, P]),
     "arches_run_batch": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P, P,
                                    P, P, P, P, P, P, C.c_int32, P, P]),
+    "arches_run_batch_async": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P,
+                                         P, P, P, P, P, P, P, C.c_int32, P, P]),
+    "arches_join": (C.c_int, [P, P]),
     "arches_switch_copy": (C.c_int, [P, C.c_int32, P, P, P, P]),
     "arches_switch_copy_one": (C.c_int, [P, P, P, C.c_size_t, P]),
     "arches_ls_materialize": (C.c_int, [P, C.c_int32, P, P, P, P]),

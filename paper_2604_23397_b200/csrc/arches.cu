@@ -70,7 +70,23 @@ struct arches_plan {
   size_t k2_tc_smem;  // 0: tensor-core K2 not applicable to this plan
   int k2_groups;      // > 1: tensor-core K2 over antenna groups of 4 (massive MIMO)
   void* dev_tables;
+  // pipelined form (arches_run_batch_async): the control tail of batch n
+  // (RNG, K3, K4) runs on `tail` next to batch n+1's K1
+  cudaStream_t tail = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_k2 = nullptr, ev_k3 = nullptr, ev_end = nullptr;
+  bool tail_pending = false;  // ev_k3 / ev_end refer to a batch not yet joined
 };
+
+// Set by arches_run_batch_async for the duration of one call: the K1 finalize
+// waits for the previous batch's K3 (it overwrites sigma2, which K3 reads) and
+// K3 is launched onto the tail stream once K2 is done.
+struct TailHook {
+  cudaEvent_t before_fin = nullptr;
+  cudaStream_t k3_stream = nullptr;
+  cudaEvent_t k2_done = nullptr;
+  bool k3_on_tail = false;
+};
+static thread_local TailHook g_hook;
 
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -489,6 +505,14 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
 extern "C" int arches_plan_destroy(arches_plan* plan) {
   if (!plan) return ARCHES_OK;
   if (plan->dev_tables) cudaFree(plan->dev_tables);
+  if (plan->tail) {
+    cudaStreamSynchronize(plan->tail);
+    cudaStreamDestroy(plan->tail);
+    cudaEventDestroy(plan->ev_start);
+    cudaEventDestroy(plan->ev_k2);
+    cudaEventDestroy(plan->ev_k3);
+    cudaEventDestroy(plan->ev_end);
+  }
   if (plan->k1t_wimg) cudaFree(plan->k1t_wimg);
   delete plan;
   return ARCHES_OK;
@@ -612,6 +636,7 @@ static int launch_k1t(const arches_plan* P, int n_units, const GridCombSrc& src,
   CUDA_TRY(ensure_smem(k1_tc<48, 40>, smem));
   k1_tc<48, 40><<<grid, K1T_THREADS, smem, s>>>(d, a, kg.n_items, tm[0], tm[1], tm[2], tm[3]);
   LAUNCH_CHECK();
+  if (g_hook.before_fin) CUDA_TRY(cudaStreamWaitEvent(s, g_hook.before_fin, 0));
   k1_tc_finalize<<<n_units, K1T_FIN_THREADS, 0, s>>>(d, a, n_units, o);
   LAUNCH_CHECK();
   return ARCHES_OK;
@@ -665,6 +690,8 @@ static int ls_analyze_impl(const arches_plan* plan, int32_t n_streams, int32_t n
           K1_NOISE | K1_MMSE | K1_AI, nullptr, seeds,
           reinterpret_cast<const unsigned char*>(state),
           state_stride_bytes(plan->dev.window_length, plan->dev.dapp_window), first_slot, n_slots};
+  if (!plan->k1t_nb && g_hook.before_fin)  // the CUDA-core K1 finalises in line
+    CUDA_TRY(cudaStreamWaitEvent(s, g_hook.before_fin, 0));
   int rc = plan->k1t_nb ? launch_k1t(plan, n_units, src, o, w, ws, s)
                         : launch_k1(plan, n_units, src, o, plan->dev.M, plan->k1_chunk, plan->k1_smem, s);
   if (rc) return rc;
@@ -756,7 +783,14 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
     kern<<<grid, TC_BLOCK, smem, s>>>(d, a, n_items, tm_y, tm_x);                            \
     LAUNCH_CHECK();                                                                          \
     /* K3 locates the (CTA, unit) segments in tile units */                                  \
-    k3_finalize<<<(n_units * 32 + K3_THREADS - 1) / K3_THREADS, K3_THREADS, 0, s>>>(         \
+    cudaStream_t s3 = s;                                                                     \
+    if (g_hook.k3_stream) {                                                                  \
+      CUDA_TRY(cudaEventRecord(g_hook.k2_done, s));                                          \
+      CUDA_TRY(cudaStreamWaitEvent(g_hook.k3_stream, g_hook.k2_done, 0));                    \
+      s3 = g_hook.k3_stream;                                                                 \
+      g_hook.k3_on_tail = true;                                                              \
+    }                                                                                        \
+    k3_finalize<<<(n_units * 32 + K3_THREADS - 1) / K3_THREADS, K3_THREADS, 0, s3>>>(        \
         d, a, n_units, n_items / ngrp, grid);                                                \
     LAUNCH_CHECK();                                                                          \
     return ARCHES_OK;                                                                        \
@@ -870,6 +904,10 @@ extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int3
   if (!plan || !seeds) return set_err(ARCHES_E_CONTRACT, "bad run_batch args");
   if (first_slot < 0 && !state)
     return set_err(ARCHES_E_CONTRACT, "first_slot < 0 needs the stream state (slot source)");
+  if (plan->tail_pending) {  // a pipelined batch is still in flight: order after it
+    const int rc = arches_join(plan, stream);
+    if (rc) return rc;
+  }
   // fork: the RNG side products (independent of the grid) on a side stream
   // next to K1; join before K2 / K3 consume them (a fork-join node pair when
   // the caller captures this into a CUDA graph)
@@ -907,6 +945,76 @@ extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int3
   if (rc) return rc;
   return arches_kpm_scan(plan, n_streams, n_slots, tel, regime, tree, state, kpm, msg_log,
                          msg_count, msg_cap, stream);
+}
+
+extern "C" int arches_join(const arches_plan* plan, arches_stream_t stream) {
+  if (!plan) return set_err(ARCHES_E_CONTRACT, "bad join args");
+  arches_plan* P = const_cast<arches_plan*>(plan);
+  if (!P->tail_pending) return ARCHES_OK;
+  CUDA_TRY(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), P->ev_end, 0));
+  P->tail_pending = false;
+  return ARCHES_OK;
+}
+
+// Cross-batch pipeline.  Per call (batch n), with T the plan's tail stream:
+//   T:      RNG(n)                         (after K4(n-1): the slot counter)
+//   stream: K1(n) -> [K3(n-1) done] -> K1 finalize(n) -> K2(n)
+//   T:      [K2(n) done] -> K3(n) -> K4(n)
+// Buffer hazards: K1 finalize(n) overwrites sigma2 (read by K3(n-1)) and K2(n)
+// the segment partials (read by K3(n-1)) -- both wait for K3(n-1); RNG(n) /
+// K3(n) overwrite rng / tel read by K3(n-1) / K4(n-1), ordered on T.  The
+// K3 / K4 of batch n thus overlap K1 of batch n+1.
+extern "C" int arches_run_batch_async(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                                      int64_t first_slot, const void* y, const void* tx,
+                                      const void* pilots, const double* noise_var,
+                                      const uint64_t* seeds, const int8_t* regime,
+                                      const arches_tree* tree, void* state, void* h_mmse,
+                                      void* h_ai, arches_telemetry* tel, arches_kpm* kpm,
+                                      arches_message* msg_log, int32_t* msg_count,
+                                      int32_t msg_cap, void* ws, arches_stream_t stream) {
+  if (!plan || !seeds) return set_err(ARCHES_E_CONTRACT, "bad run_batch_async args");
+  if (first_slot < 0 && !state)
+    return set_err(ARCHES_E_CONTRACT, "first_slot < 0 needs the stream state (slot source)");
+  arches_plan* P = const_cast<arches_plan*>(plan);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!P->tail) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(s, &cap));
+    if (cap != cudaStreamCaptureStatusNone)
+      return set_err(ARCHES_E_CONTRACT, "first run_batch_async of a plan must not be under capture");
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->tail, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_start, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_k2, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_k3, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_end, cudaEventDisableTiming));
+  }
+  struct HookGuard {
+    ~HookGuard() { g_hook = TailHook(); }
+  } guard;
+  CUDA_TRY(cudaEventRecord(P->ev_start, s));  // T follows what the caller queued so far
+  CUDA_TRY(cudaStreamWaitEvent(P->tail, P->ev_start, 0));
+  int rc = launch_rng(plan, n_streams, n_slots, seeds, first_slot, state, ws, P->tail);
+  if (rc) return rc;
+  g_hook.before_fin = P->tail_pending ? P->ev_k3 : nullptr;
+  g_hook.k3_stream = P->tail;
+  g_hook.k2_done = P->ev_k2;
+  rc = ls_analyze_impl(plan, n_streams, n_slots, y, pilots, seeds, first_slot, state, nullptr, ws,
+                       stream, false);
+  if (rc) return rc;
+  rc = experts_equalize_impl(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
+                             state, h_mmse, h_ai, tel, ws, stream, true);
+  if (rc) return rc;
+  if (!g_hook.k3_on_tail) {  // FFMA K2 path: its finalisation ran on `stream`
+    CUDA_TRY(cudaEventRecord(P->ev_k2, s));
+    CUDA_TRY(cudaStreamWaitEvent(P->tail, P->ev_k2, 0));
+  }
+  CUDA_TRY(cudaEventRecord(P->ev_k3, P->tail));
+  rc = arches_kpm_scan(plan, n_streams, n_slots, tel, regime, tree, state, kpm, msg_log,
+                       msg_count, msg_cap, reinterpret_cast<arches_stream_t>(P->tail));
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(P->ev_end, P->tail));
+  P->tail_pending = true;
+  return ARCHES_OK;
 }
 
 extern "C" int arches_switch_copy(const arches_plan* plan, int32_t n_units, const arches_kpm* kpm,

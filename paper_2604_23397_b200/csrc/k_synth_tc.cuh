@@ -400,22 +400,26 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       }
     }
   };
-  auto load_b = [&](int u, int tile, int gr, float2 (&cv)[2]) {  // coefficients rotated to the tile
+  // coefficients and the tile's phase rotation; the loads are issued one item
+  // ahead and only multiplied in write_b, so their latency hides behind the
+  // current item's epilogue
+  auto load_b = [&](int u, int tile, int gr, float2 (&cv)[4]) {
     const float2* cu = args.coef + (size_t)u * coef_stride;
     const float2* rot = P.tc_rot + (size_t)tile * (L4 + 8);
     const int bo = P.n_blocks == 1 ? 0 : min(tile * ARCHES_TILE / P.block, P.n_blocks - 1) * 8;
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-      cv[q] = boff[q] >= 0 ? cmul(__ldg(&cu[boff[q] + (bmm[q] ? bo : 0) + gr * gstr[q]]), __ldg(&rot[roff[q]]))
-                           : make_float2(0.f, 0.f);
+    for (int q = 0; q < 2; ++q) {
+      cv[2 * q] = boff[q] >= 0 ? __ldg(&cu[boff[q] + (bmm[q] ? bo : 0) + gr * gstr[q]]) : make_float2(0.f, 0.f);
+      cv[2 * q + 1] = boff[q] >= 0 ? __ldg(&rot[roff[q]]) : make_float2(0.f, 0.f);
+    }
   };
-  auto write_b = [&](int buf, const float2 (&cv)[2]) {
+  auto write_b = [&](int buf, const float2 (&cv)[4]) {
     unsigned char* bhi = sB + (size_t)buf * 2 * b_bytes;
     unsigned char* blo = bhi + b_bytes;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       if (q * TC_THREADS + (int)threadIdx.x >= n_all) break;
-      const float2 c = cv[q];
+      const float2 c = cmul(cv[2 * q], cv[2 * q + 1]);
       const float rh = tf32_rna_fast(c.x), rl = tf32_rna_fast(c.x - rh);
       const float ih = tf32_rna_fast(c.y), il = tf32_rna_fast(c.y - ih);
       *reinterpret_cast<float2*>(bhi + o0[q]) = make_float2(rh, -ih);
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
   if (lo < hi) {  // B of the first LEAD items
     int bu = u, bt = tile, bg = gr;
     for (int k = 0; k < LEAD && k < count; ++k) {
-      float2 cv[2];
+      float2 cv[4];
       load_b(bu, bt, bg, cv);
       write_b(k, cv);
       tc_fence_before();
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
     const int kk = k0 + j;
     const bool valid = kk < P.N;
     // ---- next item's data + coefficients in flight during this item's work
-    float2 cv[2];
+    float2 cv[4];
     if (has_lead) load_b(lu, lt, lg, cv);
     if constexpr (kTmap) {
       // L2 prefetch pf_dist items ahead: the shared-memory stages hold one item

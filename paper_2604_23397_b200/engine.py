@@ -201,9 +201,10 @@ class SlotEngine:
         put(self.regime, regime, np.int8)
 
     # ------------------------------------------------------------ run
-    def _launch(self, first_slot: int):
+    def _launch(self, first_slot: int, pipelined: bool = False):
         L = _lib.lib()
-        _lib.check(L.arches_run_batch(
+        fn = L.arches_run_batch_async if pipelined else L.arches_run_batch
+        _lib.check(fn(
             self.plan.handle, self.C, self.S, first_slot, _lib.ptr(self.y), _lib.ptr(self.tx),
             _lib.ptr(self.pilots), _lib.ptr(self.noise_var), _lib.ptr(self.seeds),
             _lib.ptr(self.regime), _lib.ptr(self.tree), _lib.ptr(self.state),
@@ -211,15 +212,26 @@ class SlotEngine:
             _lib.ptr(self.msg_log), _lib.ptr(self.msg_count), self.msg_cap, _lib.ptr(self.ws),
             _stream_handle()))
 
-    def run(self):
+    def run(self, pipelined: bool = False):
         """Process the loaded batch (slots next_slot .. next_slot + n_slots - 1).
         Slot numbering is read from the device-resident state, so the launch
-        sequence is identical every step and can be replayed as a CUDA graph."""
-        if self.graph is not None:
+        sequence is identical every step and can be replayed as a CUDA graph.
+
+        pipelined=True (eager only): the batch's control tail (RNG, K3, K4) is
+        left running on the plan's internal stream so it overlaps the next
+        batch's K1 (arches_run_batch_async).  Telemetry / KPM / messages /
+        state and the regime input belong to the library until join()."""
+        if pipelined:
+            self._launch(-1, pipelined=True)
+        elif self.graph is not None:
             self.graph.replay()
         else:
             self._launch(-1)
         self.next_slot += self.S
+
+    def join(self):
+        """Order the current stream after any pending pipelined tail."""
+        _lib.check(_lib.lib().arches_join(self.plan.handle, _stream_handle()))
 
     def capture_graph(self):
         """Capture one step (RNG || K1 -> K1 finalize -> K2 -> K3 -> K4) once; later run() calls replay it."""
