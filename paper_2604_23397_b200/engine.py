@@ -245,6 +245,34 @@ class SlotEngine:
         torch.cuda.current_stream().wait_stream(s)
         self.graph = g
 
+    def capture_pipeline(self, n_batches: int):
+        """CUDA graph of n_batches consecutive batches through the cross-batch
+        pipeline (arches_run_batch_async x n, then arches_join): one replay
+        processes n batches, each batch's control tail overlapping the next
+        batch's K1.  The caller advances next_slot by n_batches * n_slots per
+        replay (run_pipeline does)."""
+        import torch
+        self.join()
+        if self.plan.handle and not getattr(self, "_tail_ready", False):
+            self._launch(-1, pipelined=True)  # creates the plan's tail stream outside capture
+            self.join()
+            self.next_slot += self.S
+            self._tail_ready = True
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(n_batches):
+                    self._launch(-1, pipelined=True)
+                self.join()
+        torch.cuda.current_stream().wait_stream(s)
+        return g
+
+    def run_pipeline(self, graph, n_batches: int):
+        graph.replay()
+        self.next_slot += n_batches * self.S
+
     def launches_per_run(self) -> int:
         return 6  # RNG (forked stream), K1, K1 finalize, K2, K3, K4 (tensor-core plans)
 

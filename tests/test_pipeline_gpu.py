@@ -83,3 +83,22 @@ def test_sync_run_after_pipelined_joins_first():
     a, b = _snapshot(seq), _snapshot(mix)
     for k in a:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_graph_captured_pipeline_matches_sequential():
+    """The pipelined chain captured as one CUDA graph (bench.py's timed form)."""
+    import torch
+    geo = SlotGeometry(n_ant=4, n_prb=273)
+    seeds = [11]
+    seq = _engine(geo, 1, 32, ExecutionMode.CONCURRENT, seeds)
+    pip = _engine(geo, 1, 32, ExecutionMode.CONCURRENT, seeds)
+    g = pip.capture_pipeline(5)   # runs one batch eagerly first (creates the tail stream)
+    pip.run_pipeline(g, 5)
+    pip.run_pipeline(g, 5)
+    for _ in range(11):
+        seq.run()
+    torch.cuda.synchronize()
+    assert pip.next_slot == seq.next_slot == 11 * 32
+    a, b = _snapshot(seq), _snapshot(pip)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
