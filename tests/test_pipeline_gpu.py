@@ -43,14 +43,15 @@ def _snapshot(eng):
     }
 
 
-@pytest.mark.parametrize("n_prb,n_streams,n_slots,n_batches,exec_mode", [
-    (273, 1, 64, 12, ExecutionMode.CONCURRENT),   # config-B geometry: K3 / K4 overlap a long K1
-    (12, 3, 20, 9, ExecutionMode.CONCURRENT),     # several streams, short batches
-    (52, 2, 16, 7, ExecutionMode.SELECTED_ONLY),
+@pytest.mark.parametrize("n_prb,n_ant,n_streams,n_slots,n_batches,exec_mode", [
+    (273, 4, 1, 64, 12, ExecutionMode.CONCURRENT),   # config-B geometry: K3 / K4 overlap a long K1
+    (12, 4, 3, 20, 9, ExecutionMode.CONCURRENT),     # several streams, short batches
+    (52, 4, 2, 16, 7, ExecutionMode.SELECTED_ONLY),
+    (24, 16, 2, 8, 5, ExecutionMode.CONCURRENT),     # antenna-group K2 (massive-MIMO form)
 ])
-def test_pipelined_batches_match_sequential(n_prb, n_streams, n_slots, n_batches, exec_mode):
+def test_pipelined_batches_match_sequential(n_prb, n_ant, n_streams, n_slots, n_batches, exec_mode):
     import torch
-    geo = SlotGeometry(n_ant=4, n_prb=n_prb)
+    geo = SlotGeometry(n_ant=n_ant, n_prb=n_prb)
     seeds = [31 + 5 * k for k in range(n_streams)]
     seq = _engine(geo, n_streams, n_slots, exec_mode, seeds)
     pip = _engine(geo, n_streams, n_slots, exec_mode, seeds)
