@@ -574,13 +574,15 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       for (int d = 0; d < ND; ++d)
         h[a][d] = make_float2(vals[2 * (a * ND + d)], vals[2 * (a * ND + d) + 1]);
     float2* hout = ex ? args.h_mmse : args.h_ai;
+    // expert outputs: streaming stores (written once, never re-read by this
+    // step -- keeps them from evicting the y / tx lines still in flight)
     if (valid && half == 0 && hout) {  // half 0 stores the expert output ...
       float2* o = hout + ((size_t)u * AD + (size_t)gr * NA * ND) * P.N + kk;
 #pragma unroll
       for (int a = 0; a < NA; ++a)
         if (kStd || a < P.A)
 #pragma unroll
-          for (int d = 0; d < ND; ++d) o[(size_t)(a * ND + d) * P.N] = h[a][d];
+          for (int d = 0; d < ND; ++d) __stcs(&o[(size_t)(a * ND + d) * P.N], h[a][d]);
     }
     if (valid && half == 1) {  // ... half 1 forms its |H| telemetry
 #pragma unroll
