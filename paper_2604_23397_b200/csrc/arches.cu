@@ -72,9 +72,10 @@ struct arches_plan {
   void* dev_tables;
   // pipelined form (arches_run_batch_async): the control tail of batch n
   // (RNG, K3, K4) runs on `tail` next to batch n+1's K1
-  cudaStream_t tail = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_k2 = nullptr, ev_k3 = nullptr, ev_end = nullptr;
-  bool tail_pending = false;  // ev_k3 / ev_end refer to a batch not yet joined
+  // (mutable: execution state of a const plan, one thread at a time per plan)
+  mutable cudaStream_t tail = nullptr;
+  mutable cudaEvent_t ev_start = nullptr, ev_k2 = nullptr, ev_k3 = nullptr, ev_end = nullptr;
+  mutable bool tail_pending = false;  // ev_k3 / ev_end refer to a batch not yet joined
 };
 
 // Set by arches_run_batch_async for the duration of one call: the K1 finalize
@@ -949,7 +950,7 @@ extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int3
 
 extern "C" int arches_join(const arches_plan* plan, arches_stream_t stream) {
   if (!plan) return set_err(ARCHES_E_CONTRACT, "bad join args");
-  arches_plan* P = const_cast<arches_plan*>(plan);
+  const arches_plan* P = plan;
   if (!P->tail_pending) return ARCHES_OK;
   CUDA_TRY(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), P->ev_end, 0));
   P->tail_pending = false;
@@ -975,7 +976,7 @@ extern "C" int arches_run_batch_async(const arches_plan* plan, int32_t n_streams
   if (!plan || !seeds) return set_err(ARCHES_E_CONTRACT, "bad run_batch_async args");
   if (first_slot < 0 && !state)
     return set_err(ARCHES_E_CONTRACT, "first_slot < 0 needs the stream state (slot source)");
-  arches_plan* P = const_cast<arches_plan*>(plan);
+  const arches_plan* P = plan;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (!P->tail) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
