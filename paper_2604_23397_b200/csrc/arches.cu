@@ -490,6 +490,13 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
       sm = 2 * (size_t)(as + 1) * d.T * ARCHES_TILE * sizeof(float2) + 2 * nbuf * (size_t)d.tc_kb * ng * 256;
       if (grp) sm += (size_t)21 * TC_THREADS * sizeof(float);  // MRC sums across groups
       if (sm > 227 * 1024 || n_b > 2 * TC_THREADS || ncol > 64) sm = 0;
+      // the per-tile phase rotations in shared memory when they fit
+      const size_t rot_bytes = (size_t)d.n_tiles * (4 * d.tc_kb + 8) * sizeof(float2);
+      d.k2_rot_smem = 0;
+      if (sm && !grp && sm + rot_bytes <= 227 * 1024 && !getenv("ARCHES_K2_ROT_GLOBAL")) {
+        sm += rot_bytes;
+        d.k2_rot_smem = 1;
+      }
     }
     P->k2_tc_smem = sm;
     P->k2_groups = grp && sm ? d.A / 4 : 1;

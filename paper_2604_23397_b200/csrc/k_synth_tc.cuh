@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
   float2* sYX = reinterpret_cast<float2*>(sm);                               // [2][stage]
   unsigned char* sB = sm + 2 * stage_elems * sizeof(float2);                 // [NBUF][hi | lo]
   float* gacc = reinterpret_cast<float*>(sB + 2 * NBUF * (size_t)KB * NG * 256) + threadIdx.x;  // [21][512] (kGrp)
+  float2* srot = reinterpret_cast<float2*>(sB + 2 * NBUF * (size_t)KB * NG * 256);  // [n_tiles][L4+8] (!kGrp)
   const int n_all = (NCOL / 2) * L4;                                         // B entries
   const uint32_t ACC0 = 128;                                                 // TMEM columns
   // this thread's <= 2 B entries (output column pair r, tap l): source offsets
@@ -405,12 +406,13 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
   // current item's epilogue
   auto load_b = [&](int u, int tile, int gr, float2 (&cv)[4]) {
     const float2* cu = args.coef + (size_t)u * coef_stride;
-    const float2* rot = P.tc_rot + (size_t)tile * (L4 + 8);
+    const bool rs = !kGrp && P.k2_rot_smem;
+    const float2* rot = (rs ? srot : P.tc_rot) + (size_t)tile * (L4 + 8);
     const int bo = P.n_blocks == 1 ? 0 : min(tile * ARCHES_TILE / P.block, P.n_blocks - 1) * 8;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       cv[2 * q] = boff[q] >= 0 ? __ldg(&cu[boff[q] + (bmm[q] ? bo : 0) + gr * gstr[q]]) : make_float2(0.f, 0.f);
-      cv[2 * q + 1] = boff[q] >= 0 ? __ldg(&rot[roff[q]]) : make_float2(0.f, 0.f);
+      cv[2 * q + 1] = boff[q] < 0 ? make_float2(0.f, 0.f) : rs ? rot[roff[q]] : __ldg(&rot[roff[q]]);
     }
   };
   auto write_b = [&](int buf, const float2 (&cv)[4]) {
@@ -485,6 +487,8 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
   }
+  if (!kGrp && P.k2_rot_smem && threadIdx.x < TC_THREADS)
+    for (int i = threadIdx.x; i < n_tiles * (L4 + 8); i += TC_THREADS) srot[i] = __ldg(&P.tc_rot[i]);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
