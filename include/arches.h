@@ -10,8 +10,14 @@
  * scalars, features and accumulators are fp64.  No entry point allocates on
  * the hot path: callers own every buffer (sizes via arches_*_bytes).  Every
  * call returns an ARCHES_* status; arches_last_error() gives the thread-local
- * message.  Plans are immutable after creation and may be shared across
- * threads; work is enqueued on the caller's cudaStream_t (NULL = legacy).
+ * message.  A plan lives on the device that was current at arches_plan_create
+ * (its tables, and the internal streams of the executors) and must be used
+ * with that device current.  Threading: the per-call entry points (K1, K2, K4,
+ * K5, compat forms) only read the plan and may be called from several threads;
+ * the executors (arches_run_batch, arches_run_batch_async, arches_join) also
+ * use the plan's internal streams / pipeline state, so one thread at a time
+ * per plan for those.  Work is enqueued on the caller's cudaStream_t
+ * (NULL = legacy).
  *
  * Device layouts (unit u = stream * n_slots + slot; a stream is one
  * single-layer DMRS port of one cell; A antennas, T symbols, D DMRS symbols,
@@ -49,6 +55,12 @@ typedef struct CUstream_st* arches_stream_t; /* == cudaStream_t */
 #define ARCHES_MAX_MCS 32
 #define ARCHES_MAX_TREE_NODES 64
 #define ARCHES_MAX_PENDING 8
+
+/* arches_params.flags: force the CUDA-core forms (same results; used by the
+ * parity tests to cover the fallback kernels on geometries that would pick the
+ * tensor-core ones) */
+#define ARCHES_FLAG_NO_TC_K1 0x1 /* K1: CUDA-core comb analysis instead of tcgen05 */
+#define ARCHES_FLAG_NO_TC_K2 0x2 /* K2: FFMA synthesis/equaliser instead of tcgen05 */
 
 enum { ARCHES_EXEC_CONCURRENT = 0, ARCHES_EXEC_SELECTED_ONLY = 1 };
 enum { ARCHES_POLICY_ORACLE = 0, ARCHES_POLICY_FIXED = 1, ARCHES_POLICY_TREE = 2 };
@@ -89,7 +101,7 @@ typedef struct arches_params {
   int32_t fixed_mode;           /* policy == FIXED */
   int32_t decision_period_slots;
   int32_t dapp_window_slots;
-  int32_t reserved0;
+  int32_t flags;                /* ARCHES_FLAG_* (0 = fastest applicable kernels) */
   int64_t decision_delay_ns;    /* LatencyModel.decision_delay_ns() */
   int64_t failsafe_timeout_ns;  /* DappConfig.timeout_ns() */
   uint64_t crc_purpose_key;     /* blake2b-64("crc"), rng.py:17-21 */
@@ -243,8 +255,10 @@ int arches_run_batch(const arches_plan* plan, int32_t n_streams, int32_t n_slots
  *    arches_join(plan, stream) -- do not read or overwrite them before;
  *  - h_mmse / h_ai / y / tx / noise_var follow `stream` order as usual;
  *  - one thread at a time per plan; arches_run_batch joins a pending tail first;
- *  - a CUDA-graph capture must contain its arches_join, and the plan's first
- *    async call must happen outside capture (the internal stream is created then).
+ *  - a CUDA-graph capture must contain its arches_join;
+ *  - plans whose K2 is the FFMA form (tiles straddling MMSE blocks, n_ant 3 or
+ *    5-7, ARCHES_FLAG_NO_TC_K2) run the single-stream arches_run_batch order
+ *    (that K2 finalises on `stream` and reads the tail's RNG products).
  * Same arguments as arches_run_batch. */
 int arches_run_batch_async(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
                            int64_t first_slot, const void* y, const void* tx, const void* pilots,

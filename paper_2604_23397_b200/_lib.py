@@ -17,6 +17,7 @@ LIB_PATH = pathlib.Path(__file__).resolve().parent / "lib" / "libarches.so"
 MAX_ANT, MAX_DMRS, MAX_SYM, MAX_BINS, MAX_MCS, MAX_TREE_NODES = 64, 4, 14, 64, 32, 64
 EXEC_CONCURRENT, EXEC_SELECTED_ONLY = 0, 1
 POLICY_ORACLE, POLICY_FIXED, POLICY_TREE = 0, 1, 2
+FLAG_NO_TC_K1, FLAG_NO_TC_K2 = 0x1, 0x2
 TRIGGERS = {0: "policy", 1: "failsafe", 2: "oracle", 3: "fixed"}
 
 
@@ -37,7 +38,7 @@ class Params(C.Structure):
                 ("mcs_qam", C.c_int32 * MAX_MCS), ("mcs_rate", C.c_double * MAX_MCS),
                 ("exec_mode", C.c_int32), ("policy", C.c_int32), ("fixed_mode", C.c_int32),
                 ("decision_period_slots", C.c_int32), ("dapp_window_slots", C.c_int32),
-                ("reserved0", C.c_int32), ("decision_delay_ns", C.c_int64),
+                ("flags", C.c_int32), ("decision_delay_ns", C.c_int64),
                 ("failsafe_timeout_ns", C.c_int64), ("crc_purpose_key", C.c_uint64)]
 
 

@@ -71,15 +71,17 @@ class _PlanEntry:
         self.ws = torch.empty(plan.workspace_bytes(ws_units), dtype=torch.uint8, device="cuda")
 
 
-def _plan(geometry, guard=None, truncation=20, block_prbs=32, ds=1.25):
+def _plan(geometry, guard=None, truncation=20, block_prbs=32, ds=1.25, sinr_cap_db=60.0):
     from .engine import ArchesPlan
     if guard is None:  # unused by the caller: any valid value
         guard = max(1, min(16, 6 * geometry.n_prb - 1))
     key = (geometry.n_ant, geometry.n_prb, geometry.n_sym, tuple(geometry.dmrs_symbols),
-           float(geometry.slot_duration_us), int(guard), int(truncation), int(block_prbs), float(ds))
+           float(geometry.slot_duration_us), int(guard), int(truncation), int(block_prbs), float(ds),
+           float(sinr_cap_db))
     ent = _PLANS.get(key)
     if ent is None:
-        pc = PipelineConfig(noise_guard=guard, truncation=truncation, mmse_block_prbs=block_prbs)
+        pc = PipelineConfig(noise_guard=guard, truncation=truncation, mmse_block_prbs=block_prbs,
+                            sinr_cap_db=float(sinr_cap_db))
         try:
             plan = ArchesPlan(geometry, ds, pc, policy="fixed:1")
         except _own_errors.ConfigurationError as e:
@@ -194,11 +196,7 @@ def equalize(rx, estimate, noise_var: float, tx_grid, sinr_cap_db: float = 60.0)
         raise _E.ContractViolation("equalize expects an Interpolated estimate")
     torch = _torch()
     geo = estimate.geometry
-    ent = _plan(geo)
-    if float(sinr_cap_db) != 60.0:
-        from .engine import ArchesPlan
-        pc = PipelineConfig(sinr_cap_db=float(sinr_cap_db))
-        ent = _PlanEntry(ArchesPlan(geo, 1.25, pc, policy="fixed:1"), 1)
+    ent = _plan(geo, sinr_cap_db=sinr_cap_db)   # cached per cap like every compat plan
     y = np.asarray(rx.values)
     y_dev = torch.from_numpy(np.ascontiguousarray(np.transpose(y, (0, 2, 1)))
                              .astype(np.complex64)[None]).to("cuda")

@@ -70,11 +70,15 @@ struct arches_plan {
   size_t k2_tc_smem;  // 0: tensor-core K2 not applicable to this plan
   int k2_groups;      // > 1: tensor-core K2 over antenna groups of 4 (massive MIMO)
   void* dev_tables;
-  // pipelined form (arches_run_batch_async): the control tail of batch n
-  // (RNG, K3, K4) runs on `tail` next to batch n+1's K1
-  // (mutable: execution state of a const plan, one thread at a time per plan)
-  mutable cudaStream_t tail = nullptr;
-  mutable cudaEvent_t ev_start = nullptr, ev_k2 = nullptr, ev_k3 = nullptr, ev_end = nullptr;
+  int device;          // the CUDA device the plan (tables, streams) lives on
+  // Executor streams / events, created with the plan on its device (so no entry
+  // point creates one under graph capture).  `side`: run_batch's RNG fork.
+  // `tail`: the pipelined form (arches_run_batch_async) runs the control tail of
+  // batch n (RNG, K3, K4) there next to batch n+1's K1.
+  cudaStream_t side = nullptr, tail = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_k2 = nullptr, ev_k3 = nullptr, ev_end = nullptr;
+  // mutable: execution state of a const plan (one thread at a time per plan)
   mutable bool tail_pending = false;  // ev_k3 / ev_end refer to a batch not yet joined
 };
 
@@ -91,15 +95,19 @@ static thread_local TailHook g_hook;
 
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// cudaFuncSetAttribute is a synchronous host call: do it once per kernel (to the
-// largest value requested so far) so eager launches stay back-to-back.
+// cudaFuncSetAttribute is a synchronous host call: do it once per (device,
+// kernel) (to the largest value requested so far) so eager launches stay
+// back-to-back.
 template <typename K>
 static cudaError_t ensure_smem(K kern, size_t smem) {
   static std::mutex mu;
-  static std::map<const void*, size_t> set_to;  // per kernel function
+  static std::map<std::pair<int, const void*>, size_t> set_to;  // per device and kernel
   if (smem <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e0 = cudaGetDevice(&dev);
+  if (e0 != cudaSuccess) return e0;
   std::lock_guard<std::mutex> lk(mu);
-  size_t& cur = set_to[reinterpret_cast<const void*>(kern)];
+  size_t& cur = set_to[{dev, reinterpret_cast<const void*>(kern)}];
   if (smem <= cur) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) cur = smem;
@@ -219,6 +227,25 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
   if (p.window_length < 1 || p.dapp_window_slots < 1 || p.decision_period_slots < 1)
     return set_err(ARCHES_E_CONFIG, "window lengths and periods must be positive");
   if (p.assumed_delay_spread < 0) return set_err(ARCHES_E_CONFIG, "delay_spread must be >= 0");
+  if (p.flags & ~(ARCHES_FLAG_NO_TC_K1 | ARCHES_FLAG_NO_TC_K2))
+    return set_err(ARCHES_E_CONFIG, "unknown flags 0x%x", (unsigned)p.flags);
+  {
+    // The device keeps in-flight control messages in fixed queues of
+    // ARCHES_MAX_PENDING (the reference list is unbounded, phy_pipeline.py:
+    // 114-117).  A message emitted at the end of slot n is applied at
+    // n + 1 + ceil(delay / slot) (+1 selected-only); one is emitted per
+    // decision period, so at most ceil(delay / (period * slot)) + 2 are in
+    // flight.  Reject the configurations that could exceed the queue.
+    const double slot_ns = g.slot_duration_us * 1000.0;
+    const double per = (double)p.decision_period_slots * slot_ns;
+    const double need = ceil((double)std::max<int64_t>(p.decision_delay_ns, 0) / per) + 2.0;
+    if (p.policy == ARCHES_POLICY_TREE && need > ARCHES_MAX_PENDING)
+      return set_err(ARCHES_E_CONFIG,
+                     "decision delay %lld ns over a %d-slot period keeps up to %.0f control "
+                     "messages in flight; the device queue holds %d",
+                     (long long)p.decision_delay_ns, p.decision_period_slots, need,
+                     ARCHES_MAX_PENDING);
+  }
 
   arches_plan* P = new arches_plan();
   memset(P, 0, sizeof(*P));
@@ -395,8 +422,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     d.num_sms = sms > 0 ? sms : 148;
-    const char* pf = getenv("ARCHES_K2_PREFETCH");
-    d.pf_dist = pf ? atoi(pf) : 0;  // measured: no gain at 1-3 (K2 is not HBM-latency bound)
+    P->device = dev;
   }
 
   // ---- K1 launch geometry
@@ -417,7 +443,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
     P->k1t_nchunks = (N + K1T_CSC - 1) / K1T_CSC;
     const int nb = ((2 * d.L + 15) / 16) * 16;
     if (d.diag && d.D <= 4 && d.L == 20 && P->k1t_nchunks <= K1T_MAX_CHUNKS &&
-        !getenv("ARCHES_DISABLE_K1T")) {  // k1_tc<48, 40>
+        !(p.flags & ARCHES_FLAG_NO_TC_K1)) {  // k1_tc<48, 40>
       // chunk-invariant operand W[p][l] = e^{2 pi i l p / M} (p < 16 comb points),
       // real-embedded: kappa = 2p + (0: Re h, 1: Im h), row n = 2l + (0: Re, 1: Im);
       // [n][32 floats] in the SWIZZLE_128B layout, tf32 hi then lo
@@ -482,7 +508,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
     const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : d.A <= 4 ? 4 : grp ? 4 : 0;
     const bool tile_ok = d.n_blocks == 1 || (d.block % ARCHES_TILE) == 0;
     size_t sm = 0;
-    if (na && tile_ok && 16 * d.tc_kb <= 128 && !getenv("ARCHES_DISABLE_TC")) {
+    if (na && tile_ok && 16 * d.tc_kb <= 128 && !(p.flags & ARCHES_FLAG_NO_TC_K2)) {
       const int R = 2 * na * d.D, ncol = ((2 * R + 15) / 16) * 16, ng = ncol / 8;
       const int n_b = (ncol / 2) * 4 * d.tc_kb;  // B entries: <= 2 per thread of 512
       const int as = grp ? 4 : d.A;               // antennas per stage
@@ -493,7 +519,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
       // the per-tile phase rotations in shared memory when they fit
       const size_t rot_bytes = (size_t)d.n_tiles * (4 * d.tc_kb + 8) * sizeof(float2);
       d.k2_rot_smem = 0;
-      if (sm && !grp && sm + rot_bytes <= 227 * 1024 && !getenv("ARCHES_K2_ROT_GLOBAL")) {
+      if (sm && !grp && sm + rot_bytes <= 227 * 1024) {
         sm += rot_bytes;
         d.k2_rot_smem = 1;
       }
@@ -503,8 +529,21 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
   }
   if (P->k2_smem > 200 * 1024 && !(P->k2_tc_smem && P->k2_groups > 1)) {
     cudaFree(buf);
+    if (P->k1t_wimg) cudaFree(P->k1t_wimg);
     delete P;
     return set_err(ARCHES_E_CONFIG, "K2 tile does not fit shared memory (n_ant too large)");
+  }
+  if (cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&P->tail, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&P->ev_start, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&P->ev_k2, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&P->ev_k3, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&P->ev_end, cudaEventDisableTiming) != cudaSuccess) {
+    const cudaError_t e = cudaGetLastError();
+    arches_plan_destroy(P);
+    return set_err(ARCHES_E_CUDA, "plan streams/events: %s", cudaGetErrorString(e));
   }
   *out = P;
   return ARCHES_OK;
@@ -512,16 +551,20 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
 
 extern "C" int arches_plan_destroy(arches_plan* plan) {
   if (!plan) return ARCHES_OK;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != plan->device) cudaSetDevice(plan->device);
+  for (cudaStream_t st : {plan->tail, plan->side})
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  for (cudaEvent_t ev : {plan->ev_fork, plan->ev_join, plan->ev_start, plan->ev_k2, plan->ev_k3,
+                         plan->ev_end})
+    if (ev) cudaEventDestroy(ev);
   if (plan->dev_tables) cudaFree(plan->dev_tables);
-  if (plan->tail) {
-    cudaStreamSynchronize(plan->tail);
-    cudaStreamDestroy(plan->tail);
-    cudaEventDestroy(plan->ev_start);
-    cudaEventDestroy(plan->ev_k2);
-    cudaEventDestroy(plan->ev_k3);
-    cudaEventDestroy(plan->ev_end);
-  }
   if (plan->k1t_wimg) cudaFree(plan->k1t_wimg);
+  if (cur >= 0 && cur != plan->device) cudaSetDevice(cur);
   delete plan;
   return ARCHES_OK;
 }
@@ -618,29 +661,6 @@ static int launch_k1t(const arches_plan* P, int n_units, const GridCombSrc& src,
       return set_err(ARCHES_E_CUDA, "K1: tensor map encode failed");
   const int grid = std::min(kg.n_items, d.num_sms);
   const size_t smem = k1t_smem_bytes(a.nb);
-  a.dbg = nullptr;
-  static long long* dbg_buf = nullptr;
-  const bool dbg = getenv("ARCHES_K1T_DBG") != nullptr;  // profiling aid: wait cycles per role
-  if (dbg) {
-    if (!dbg_buf) cudaMalloc(&dbg_buf, 1024 * 8 * sizeof(long long));
-    cudaMemsetAsync(dbg_buf, 0, 1024 * 8 * sizeof(long long), s);
-    a.dbg = dbg_buf;
-  }
-  struct DbgPrint {
-    bool on; long long* buf; int g; cudaStream_t s;
-    ~DbgPrint() {
-      if (!on) return;
-      std::vector<long long> h(g * 8);
-      cudaStreamSynchronize(s);
-      cudaMemcpy(h.data(), buf, g * 8 * sizeof(long long), cudaMemcpyDeviceToHost);
-      double acc[8] = {0};
-      for (int b = 0; b < g; ++b)
-        for (int k = 0; k < 8; ++k) acc[k] += (double)h[b * 8 + k] / g;
-      fprintf(stderr, "k1t waits (cycles/CTA): prod.empty %.0f | mma.acce %.0f mma.conv %.0f | "
-              "conv.accf %.0f conv.full %.0f conv.mfree %.0f | conv total %.0f\n",
-              acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6]);
-    }
-  } dbg_print{dbg, dbg_buf, grid, s};
   CUDA_TRY(ensure_smem(k1_tc<48, 40>, smem));
   k1_tc<48, 40><<<grid, K1T_THREADS, smem, s>>>(d, a, kg.n_items, tm[0], tm[1], tm[2], tm[3]);
   LAUNCH_CHECK();
@@ -781,8 +801,8 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
   CUtensorMap tm_y, tm_x;
   memset(&tm_y, 0, sizeof(tm_y));
   memset(&tm_x, 0, sizeof(tm_x));
-  const bool tmap = getenv("ARCHES_K2_NO_TMAP") == nullptr &&
-                    make_row_tmap(&tm_y, a.y, d.N, d.A * d.T, n_units, ngrp > 1 ? 4 * d.T : 0) &&
+  // tensor maps need 16-byte aligned bases; otherwise the CUDA-core loads
+  const bool tmap = make_row_tmap(&tm_y, a.y, d.N, d.A * d.T, n_units, ngrp > 1 ? 4 * d.T : 0) &&
                     make_row_tmap(&tm_x, a.tx, d.N, d.T, n_units);
 #define K2TC_LAUNCH_G(NA_, ND_, STD_, GRP_)                                                  \
   {                                                                                          \
@@ -916,38 +936,21 @@ extern "C" int arches_run_batch(const arches_plan* plan, int32_t n_streams, int3
     const int rc = arches_join(plan, stream);
     if (rc) return rc;
   }
-  // fork: the RNG side products (independent of the grid) on a side stream
-  // next to K1; join before K2 / K3 consume them (a fork-join node pair when
-  // the caller captures this into a CUDA graph)
-  static thread_local cudaStream_t side = nullptr;
-  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // fork: the RNG side products (independent of the grid) on the plan's side
+  // stream next to K1; join before K2 / K3 consume them (a fork-join node pair
+  // when the caller captures this into a CUDA graph)
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (!side) {
-    // streams / events cannot be created while `stream` is being captured: the
-    // first call made inside a capture runs the RNG in line instead
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    CUDA_TRY(cudaStreamIsCapturing(s, &cap));
-    if (cap == cudaStreamCaptureStatusNone) {
-      CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-      CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-      CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    }
-  }
-  int rc;
-  if (side) {
-    CUDA_TRY(cudaEventRecord(ev_fork, s));
-    CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
-    rc = launch_rng(plan, n_streams, n_slots, seeds, first_slot, state, ws, side);
-    if (rc) return rc;
-    CUDA_TRY(cudaEventRecord(ev_join, side));
-  } else {
-    rc = launch_rng(plan, n_streams, n_slots, seeds, first_slot, state, ws, s);
-    if (rc) return rc;
-  }
+  cudaStream_t side = plan->side;
+  cudaEvent_t ev_fork = plan->ev_fork, ev_join = plan->ev_join;
+  CUDA_TRY(cudaEventRecord(ev_fork, s));
+  CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
+  int rc = launch_rng(plan, n_streams, n_slots, seeds, first_slot, state, ws, side);
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(ev_join, side));
   rc = ls_analyze_impl(plan, n_streams, n_slots, y, pilots, seeds, first_slot, state, nullptr, ws,
                        stream, false);
   if (rc) return rc;
-  if (side) CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
+  CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
   rc = experts_equalize_impl(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
                              state, h_mmse, h_ai, tel, ws, stream, /* RNG side products */ true);
   if (rc) return rc;
@@ -985,16 +988,14 @@ extern "C" int arches_run_batch_async(const arches_plan* plan, int32_t n_streams
     return set_err(ARCHES_E_CONTRACT, "first_slot < 0 needs the stream state (slot source)");
   const arches_plan* P = plan;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (!P->tail) {
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    CUDA_TRY(cudaStreamIsCapturing(s, &cap));
-    if (cap != cudaStreamCaptureStatusNone)
-      return set_err(ARCHES_E_CONTRACT, "first run_batch_async of a plan must not be under capture");
-    CUDA_TRY(cudaStreamCreateWithFlags(&P->tail, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_start, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_k2, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_k3, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_end, cudaEventDisableTiming));
+  if (!P->k2_tc_smem) {
+    // The FFMA K2 finalises its units in its last CTA on `stream`: it reads the
+    // RNG side products and writes tel, both owned by the tail stream in the
+    // pipelined form.  Such plans (tiles straddling MMSE blocks, n_ant 3 / 5-7)
+    // run the ordered single-stream form instead -- same results.
+    return arches_run_batch(plan, n_streams, n_slots, first_slot, y, tx, pilots, noise_var, seeds,
+                            regime, tree, state, h_mmse, h_ai, tel, kpm, msg_log, msg_count,
+                            msg_cap, ws, stream);
   }
   struct HookGuard {
     ~HookGuard() { g_hook = TailHook(); }
@@ -1012,10 +1013,7 @@ extern "C" int arches_run_batch_async(const arches_plan* plan, int32_t n_streams
   rc = experts_equalize_impl(plan, n_streams, n_slots, y, tx, noise_var, seeds, first_slot,
                              state, h_mmse, h_ai, tel, ws, stream, true);
   if (rc) return rc;
-  if (!g_hook.k3_on_tail) {  // FFMA K2 path: its finalisation ran on `stream`
-    CUDA_TRY(cudaEventRecord(P->ev_k2, s));
-    CUDA_TRY(cudaStreamWaitEvent(P->tail, P->ev_k2, 0));
-  }
+  if (!g_hook.k3_on_tail) return set_err(ARCHES_E_STATE, "pipelined K3 was not placed on the tail");
   CUDA_TRY(cudaEventRecord(P->ev_k3, P->tail));
   rc = arches_kpm_scan(plan, n_streams, n_slots, tel, regime, tree, state, kpm, msg_log,
                        msg_count, msg_cap, reinterpret_cast<arches_stream_t>(P->tail));

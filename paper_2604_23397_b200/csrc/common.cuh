@@ -35,7 +35,6 @@ struct PlanDev {
   int tc_kb;                    // its 8-wide K blocks (Lsyn / 4)
   const float2* tc_rot;         // [n_tiles][4*tc_kb + 8]: e^{-2 pi i l k0/N} (AI), e^{-2 pi i l (k0-b*block)/N} (MMSE)
   int num_sms;
-  int pf_dist;                  // K2 L2 prefetch distance in CTAs (0 = off)
   int k2_rot_smem;              // tensor-core K2 stages tc_rot in shared memory
   // KPM layer
   double sinr_cap_db, lcid4_fraction, lcid4_jitter, crc_margin_db, crc_scale_db;

@@ -49,7 +49,6 @@ struct K1TArgs {
   int n_slots, n_rows;     // rows = units * A
   int n_g, parts, cpp;     // row tiles, subcarrier parts, chunks per part
   int n_chunks, nb;        // chunks per row, MMA N
-  long long* dbg;          // profiling aid: per-CTA wait cycles [G][8] (null = off)
 };
 
 // RNG side products of each unit (Philox CRC uniform of rng.stream(seed, "crc",
@@ -71,8 +70,6 @@ __global__ void k_rng_units(const PlanDev P, double* rng, const uint64_t* seeds,
   const double f = __dadd_rn(P.lcid4_fraction, __dmul_rn(P.lcid4_jitter, jit));
   rng[2 * u + 1] = fmin(fmax(f, 0.0), 1.0);
 }
-#define K1T_T0() long long t0_ = a.dbg ? clock64() : 0
-#define K1T_T1(slot) if (a.dbg) atomicAdd((unsigned long long*)&a.dbg[blockIdx.x * 8 + (slot)], (unsigned long long)(clock64() - t0_))
 
 constexpr uint32_t K1T_ATOM = 128 * 128;           // 128 rows x 128 B (one SWIZZLE_128B K block)
 constexpr uint32_t K1T_RAW_BYTES = 2 * K1T_ATOM;    // raw chunk: 32 subcarriers of 128 rows
@@ -174,9 +171,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
         for (int c = c0; c < c1; ++c, ++j) {
           const int s = j % K1T_STAGES;
           if (j >= K1T_STAGES) {
-            K1T_T0();
             mbar_wait_spin(&s_empty[s], ((j / K1T_STAGES) - 1) & 1);
-            K1T_T1(0);
           }
           mbar_arrive_expect_tx(&s_full[s], K1T_RAW_BYTES);
           unsigned char* dst = raw + (size_t)s * K1T_RAW_BYTES;
@@ -201,14 +196,10 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
         for (int c = c0; c < c1; ++c, ++j) {
           const int b = j % K1T_MBUF, r = j % K1T_ACC;
           {
-            K1T_T0();
             if (j >= K1T_ACC) mbar_wait_spin(&s_acce[r], ((j / K1T_ACC) - 1) & 1);
-            K1T_T1(1);
           }
           {
-            K1T_T0();
             mbar_wait_spin(&s_conv[b], (j / K1T_MBUF) & 1);
-            K1T_T1(2);
           }
           tc_fence_after();
           const uint32_t dcol = tmem + (uint32_t)(r * nb);
@@ -252,9 +243,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
       for (int c = c0; c < c1; ++c, ++j) {
         const int r = j % K1T_ACC;
         {
-          K1T_T0();
           mbar_wait_spin(&s_accf[r], (j / K1T_ACC) & 1);
-          if (t == 0) K1T_T1(3);
         }
         tc_fence_after();
         float vals[NB];
@@ -297,7 +286,6 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
 #pragma unroll
   for (int k = 0; k < 8; ++k) swz[k] = ((uint32_t)k ^ sw) * 16u;
   int j = 0;
-  const long long t_start = clock64();
   for (int item = blockIdx.x; item < n_items; item += G) {
     int g, d, c0, c1;
     item_chunks(item, g, d, c0, c1);
@@ -325,14 +313,10 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
       for (int k = 0; k < K1T_CP; ++k) qv[k] = qn[k];
       load_pilots(c + 1);
       {
-        K1T_T0();
         mbar_wait_spin(&s_full[s], (j / K1T_STAGES) & 1);
-        if (threadIdx.x == 0) K1T_T1(4);
       }
       {
-        K1T_T0();
         if (j >= K1T_MBUF) mbar_wait_spin(&s_mfree[b], ((j / K1T_MBUF) - 1) & 1);
-        if (threadIdx.x == 0) K1T_T1(5);
       }
       // row t, 16-byte group k of atom a at a*16K + t*128 + (k ^ (t & 7))*16
       // (SWIZZLE_128B); group = (y[2m].re, .im, y[2m+1].re, .im), m = 16c + 8a + k
@@ -372,7 +356,6 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
     }
     if (live) a.epart[(size_t)item * 128 + t] = e64;
   }
-  if (a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 8 + 6] = clock64() - t_start;
   // TMEM is released once the drain warps have read their last accumulator
   named_bar(2, 2 * NT);
   tc_fence_after();

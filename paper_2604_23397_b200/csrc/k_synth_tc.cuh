@@ -550,21 +550,6 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
     // ---- next item's data + coefficients in flight during this item's work
     float2 cv[4];
     if (has_lead) load_b(lu, lt, lg, cv);
-    if constexpr (kTmap) {
-      // L2 prefetch pf_dist items ahead: the shared-memory stages hold one item
-      // in flight, the L2 holds the next ones (tensor-map prefetch, one
-      // instruction per operand)
-      const int pf = item + 1 + P.pf_dist;
-      if (!kGrp && P.pf_dist > 0 && threadIdx.x == 32 && pf < hi) {
-        const int pu = pf / n_tiles, pt = pf - pu * n_tiles;
-        asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
-                         reinterpret_cast<uint64_t>(&tm_y)), "r"(pt * 2 * ARCHES_TILE), "r"(0), "r"(pu)
-                     : "memory");
-        asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
-                         reinterpret_cast<uint64_t>(&tm_x)), "r"(pt * 2 * ARCHES_TILE), "r"(0), "r"(pu)
-                     : "memory");
-      }
-    }
     // ---- this expert's synthesised taps
     mbar_wait(&s_mma[mb], mph);
     tc_fence_after();

@@ -41,7 +41,8 @@ class ArchesPlan:
 
     def __init__(self, geometry, assumed_delay_spread: float, pcfg: PipelineConfig | None = None,
                  exec_mode: ExecutionMode = ExecutionMode.CONCURRENT, policy: str = "oracle",
-                 dapp: DappConfig | None = None, latency: LatencyModel | None = None):
+                 dapp: DappConfig | None = None, latency: LatencyModel | None = None,
+                 flags: int = 0):
         if getattr(geometry, "n_layers", 1) != 1:
             raise ConfigurationError("estimators support a single layer (one plan per layer port)")
         pcfg = pcfg or PipelineConfig()
@@ -88,6 +89,7 @@ class ArchesPlan:
         p.decision_delay_ns = latency.decision_delay_ns()
         p.failsafe_timeout_ns = dapp.timeout_ns(geometry.slot_duration_ns)
         p.crc_purpose_key = purpose_key("crc")
+        p.flags = int(flags)   # _lib.FLAG_NO_TC_K1 / FLAG_NO_TC_K2: force the CUDA-core kernels
         self._geom, self._params = g, p
         h = C.c_void_p()
         _lib.check(_lib.lib().arches_plan_create(C.byref(g), C.byref(p), C.byref(h)))
@@ -160,10 +162,18 @@ class SlotEngine:
             raise ConfigurationError("tree policy needs a tree")
         self.next_slot = 0
         self.graph = None
+        self._pending = False   # a pipelined tail (RNG/K3/K4) may still own tel/kpm/state/regime
         self.reset()
 
     # ------------------------------------------------------------ state
+    def _settle(self):
+        """Order the current stream after a pending pipelined tail before touching
+        anything the tail owns (arches_run_batch_async contract, include/arches.h)."""
+        if self._pending:
+            self.join()
+
     def reset(self):
+        self._settle()
         _lib.check(_lib.lib().arches_state_init(self.plan.handle, _lib.ptr(self.state), self.C,
                                                 _stream_handle()))
         self.msg_count.zero_()
@@ -186,6 +196,7 @@ class SlotEngine:
         y: (U, A, T, N) complex64 device layout; tx: (U, T, N); noise_var: (U,);
         regime: (U,) 1 = good."""
         import torch
+        self._settle()   # K4(n-1) may still read regime / noise_var
 
         def put(dst, src, dtype):
             if src is None:
@@ -223,6 +234,7 @@ class SlotEngine:
         state and the regime input belong to the library until join()."""
         if pipelined:
             self._launch(-1, pipelined=True)
+            self._pending = True
         elif self.graph is not None:
             self.graph.replay()
         else:
@@ -232,6 +244,7 @@ class SlotEngine:
     def join(self):
         """Order the current stream after any pending pipelined tail."""
         _lib.check(_lib.lib().arches_join(self.plan.handle, _stream_handle()))
+        self._pending = False
 
     def capture_graph(self):
         """Capture one step (RNG || K1 -> K1 finalize -> K2 -> K3 -> K4) once; later run() calls replay it."""
@@ -253,11 +266,6 @@ class SlotEngine:
         replay (run_pipeline does)."""
         import torch
         self.join()
-        if self.plan.handle and not getattr(self, "_tail_ready", False):
-            self._launch(-1, pipelined=True)  # creates the plan's tail stream outside capture
-            self.join()
-            self.next_slot += self.S
-            self._tail_ready = True
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         g = torch.cuda.CUDAGraph()
@@ -278,21 +286,25 @@ class SlotEngine:
 
     def switch_copy(self):
         """K5: reference aliasing semantics -- copy MMSE into the AI buffer for mode-1 units."""
+        self._settle()
         _lib.check(_lib.lib().arches_switch_copy(self.plan.handle, self.U, _lib.ptr(self.kpm),
                                                  _lib.ptr(self.h_mmse), _lib.ptr(self.h_ai),
                                                  _stream_handle()))
 
     # ------------------------------------------------------------ results
     def kpm_records(self) -> np.ndarray:
+        self._settle()
         return self.kpm.cpu().numpy().view(_lib.KPM_DTYPE).reshape(self.C, self.S)
 
     def telemetry(self) -> np.ndarray:
+        self._settle()
         return self.tel.cpu().numpy().view(_lib.TELEMETRY_DTYPE).reshape(self.C, self.S)
 
     def messages(self, stream: int = 0) -> np.ndarray:
         """Control messages of one stream in emission order (ControlMessage log of
         execute_run, harness.py:184-226).  The fixed policy's t=0 message is a
         configuration event and is reported first."""
+        self._settle()
         n = int(self.msg_count[stream].item())
         raw = self.msg_log.view(self.C, -1)[stream].cpu().numpy().view(_lib.MESSAGE_DTYPE)
         out = raw[:min(n, self.msg_cap)]

@@ -62,3 +62,22 @@ def test_error_codes_map_onto_reference_classes():
     assert issubclass(E.ConfigurationError, ValueError)
     assert issubclass(E.ContractViolation, ValueError)
     assert issubclass(E.EstimatorError, RuntimeError)
+
+
+def test_plan_rejects_control_queues_the_device_cannot_hold():
+    """A decision delay spanning more decision periods than the device's
+    in-flight message queue (ARCHES_MAX_PENDING) is a configuration error at
+    plan creation (the check runs before any device call), never a silently
+    dropped message (the reference list is unbounded, phy_pipeline.py:114-117)."""
+    import pytest
+    from paper_2604_23397_b200 import errors as E
+    from paper_2604_23397_b200.config import DappConfig, LatencyModel
+    from paper_2604_23397_b200.engine import ArchesPlan
+    from paper_2604_23397_b200.geometry import SlotGeometry
+    geo = SlotGeometry(n_ant=2, n_prb=4)
+    # 10 ms of framework latency at a 1-slot decision period: ~20 messages in flight
+    lat = LatencyModel(framework_overhead_us=10_000.0)
+    with pytest.raises(E.ConfigurationError, match="in flight"):
+        ArchesPlan(geo, 1.25, policy="tree", dapp=DappConfig(decision_period_slots=1,
+                                                              window_length_slots=1),
+                   latency=lat)

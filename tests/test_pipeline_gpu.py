@@ -13,7 +13,7 @@ from paper_2604_23397_b200.scene import CellScene, to_device_layout
 pytestmark = pytest.mark.gpu
 
 
-def _engine(geo, n_streams, n_slots, exec_mode, seeds):
+def _engine(geo, n_streams, n_slots, exec_mode, seeds, flags=0, pcfg=None):
     from paper_2604_23397_b200.engine import ArchesPlan, SlotEngine
     streams = []
     for k, seed in enumerate(seeds):
@@ -21,7 +21,8 @@ def _engine(geo, n_streams, n_slots, exec_mode, seeds):
         regimes = ["good" if ((i + k) // 3) % 2 == 0 else "poor" for i in range(n_slots)]
         cs = CellScene(geo, scens, regimes[0])
         streams.append((cs, regimes, [cs.next_slot(r) for r in regimes]))
-    plan = ArchesPlan(geo, 1.25, PipelineConfig(window_length=8), exec_mode, "oracle")
+    plan = ArchesPlan(geo, 1.25, pcfg or PipelineConfig(window_length=8), exec_mode, "oracle",
+                      flags=flags)
     eng = SlotEngine(plan, n_streams, n_slots)
     eng.set_streams(np.stack([s[0].pilots for s in streams]), seeds)
     eng.load(y=np.stack([to_device_layout(sl.y) for s in streams for sl in s[2]]),
@@ -43,18 +44,27 @@ def _snapshot(eng):
     }
 
 
-@pytest.mark.parametrize("n_prb,n_ant,n_streams,n_slots,n_batches,exec_mode", [
-    (273, 4, 1, 64, 12, ExecutionMode.CONCURRENT),   # config-B geometry: K3 / K4 overlap a long K1
-    (12, 4, 3, 20, 9, ExecutionMode.CONCURRENT),     # several streams, short batches
-    (52, 4, 2, 16, 7, ExecutionMode.SELECTED_ONLY),
-    (24, 16, 2, 8, 5, ExecutionMode.CONCURRENT),     # antenna-group K2 (massive-MIMO form)
+FFMA = 0x3   # _lib.FLAG_NO_TC_K1 | FLAG_NO_TC_K2: the CUDA-core K1 and the FFMA K2
+
+
+@pytest.mark.parametrize("n_prb,n_ant,n_streams,n_slots,n_batches,exec_mode,flags,block", [
+    (273, 4, 1, 64, 12, ExecutionMode.CONCURRENT, 0, 32),   # config-B geometry: K3 / K4 overlap a long K1
+    (12, 4, 3, 20, 9, ExecutionMode.CONCURRENT, 0, 32),     # several streams, short batches
+    (52, 4, 2, 16, 7, ExecutionMode.SELECTED_ONLY, 0, 32),
+    (24, 16, 2, 8, 5, ExecutionMode.CONCURRENT, 0, 32),     # antenna-group K2 (massive-MIMO form)
+    # FFMA K2 plans (finalise on the caller's stream): routed to the ordered form
+    (12, 6, 2, 16, 5, ExecutionMode.CONCURRENT, 0, 32),     # n_ant 6: no tensor-core K2
+    (64, 4, 1, 16, 6, ExecutionMode.CONCURRENT, 0, 16),     # tiles straddle 16-PRB MMSE blocks
+    (52, 4, 2, 16, 6, ExecutionMode.SELECTED_ONLY, FFMA, 32),
 ])
-def test_pipelined_batches_match_sequential(n_prb, n_ant, n_streams, n_slots, n_batches, exec_mode):
+def test_pipelined_batches_match_sequential(n_prb, n_ant, n_streams, n_slots, n_batches, exec_mode,
+                                            flags, block):
     import torch
     geo = SlotGeometry(n_ant=n_ant, n_prb=n_prb)
     seeds = [31 + 5 * k for k in range(n_streams)]
-    seq = _engine(geo, n_streams, n_slots, exec_mode, seeds)
-    pip = _engine(geo, n_streams, n_slots, exec_mode, seeds)
+    pc = PipelineConfig(window_length=8, mmse_block_prbs=block)
+    seq = _engine(geo, n_streams, n_slots, exec_mode, seeds, flags, pc)
+    pip = _engine(geo, n_streams, n_slots, exec_mode, seeds, flags, pc)
     for _ in range(n_batches):
         seq.run()
     for _ in range(n_batches):
@@ -93,13 +103,50 @@ def test_graph_captured_pipeline_matches_sequential():
     seeds = [11]
     seq = _engine(geo, 1, 32, ExecutionMode.CONCURRENT, seeds)
     pip = _engine(geo, 1, 32, ExecutionMode.CONCURRENT, seeds)
-    g = pip.capture_pipeline(5)   # runs one batch eagerly first (creates the tail stream)
+    g = pip.capture_pipeline(5)   # the plan's streams exist from creation: nothing runs eagerly
     pip.run_pipeline(g, 5)
     pip.run_pipeline(g, 5)
-    for _ in range(11):
+    for _ in range(10):
         seq.run()
     torch.cuda.synchronize()
-    assert pip.next_slot == seq.next_slot == 11 * 32
+    assert pip.next_slot == seq.next_slot == 10 * 32
     a, b = _snapshot(seq), _snapshot(pip)
     for k in a:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_streaming_load_between_pipelined_batches():
+    """load() of the next batch while the previous batch's tail (K4 reads the
+    regime timeline) may still run: the engine joins the tail first, so a
+    streaming loop (load, run pipelined, load, ...) equals the sequential one."""
+    import torch
+    geo = SlotGeometry(n_ant=4, n_prb=52)
+    seeds = [19]
+    scens = default_scenarios(seeds[0], geo)
+    n_slots, n_batches = 16, 6
+    regimes = ["good" if (i // 5) % 2 == 0 else "poor" for i in range(n_slots * n_batches)]
+    cs = CellScene(geo, scens, regimes[0])
+    slots = [cs.next_slot(r) for r in regimes]
+
+    def batch(b):
+        sl = slots[b * n_slots:(b + 1) * n_slots]
+        rg = regimes[b * n_slots:(b + 1) * n_slots]
+        return dict(y=np.stack([to_device_layout(x.y) for x in sl]),
+                    tx=np.stack([x.tx.T for x in sl]).astype(np.complex64),
+                    noise_var=[x.noise_var for x in sl], regime=[1 if r == "good" else 0 for r in rg])
+
+    from paper_2604_23397_b200.engine import ArchesPlan, SlotEngine
+    out = []
+    for pipelined in (False, True):
+        plan = ArchesPlan(geo, 1.25, PipelineConfig(window_length=8), ExecutionMode.CONCURRENT,
+                          "oracle")
+        eng = SlotEngine(plan, 1, n_slots)
+        eng.set_streams(cs.pilots[None], seeds)
+        for b in range(n_batches):   # nothing read back in between: only load() joins
+            eng.load(**batch(b))
+            eng.run(pipelined=pipelined)
+        torch.cuda.synchronize()
+        out.append((eng.kpm_records().copy(), eng.messages().copy(), eng.state.cpu().numpy()))
+    for x, y in zip(out[0], out[1]):
+        assert np.array_equal(x, y)
+    assert len(out[0][1]) >= 8   # the regime timeline drove mode changes in every batch

@@ -1,0 +1,70 @@
+"""Long closed-loop golden traces from the UNMODIFIED reference (build container only).
+
+Run from the repo root:  python tools/make_golden_long.py [loop_id ...]
+Writes tests/golden/loops_long.npz / loops_long.json (one entry per loop; an
+existing file is merged so loops can be generated separately).
+
+These pin the BENCHED shapes themselves (VERDICT r1 "next" item 1):
+  p273_alt_w100_conc  -- config B: 273 PRB, 4 RX, good/poor alternating every slot,
+                         oracle policy, concurrent, DEFAULT window_length = 100,
+                         320 slots (windows wrap three times; crosses K4's 256-slot
+                         chunk boundary and the bench's 256-slot batch boundary)
+  p273_alt_w100_sel   -- the same in selected-only mode, 300 slots
+  p52_tree_default    -- config A: 52 PRB, 4 RX, tree policy with the DEFAULT dApp
+                         (decision period 100, window 100), 600 slots G/P/G
+Recorded: KPM rows (KpmRecord.row(), phy_pipeline.py:291-310), per-slot
+post-eq SINR / |H| mean / CRC, modes, control messages, fail-safe events
+(harness.execute_run, harness.py:174-231).
+"""
+from __future__ import annotations
+
+import json
+import pathlib
+import sys
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT / "tools"))
+import make_golden as MG  # noqa: E402  (loads the reference through ref_shim)
+
+PP, SP = MG.PP, MG.SP
+OUT = MG.OUT
+G, P = "good", "poor"
+
+
+def loops():
+    conc, sel = PP.ExecutionMode.CONCURRENT, PP.ExecutionMode.SELECTED_ONLY
+    alt = lambda n: tuple((G if i % 2 == 0 else P, 1) for i in range(n))  # noqa: E731
+    return {
+        "p273_alt_w100_conc": (MG.std_spec(273, alt(320), 31, conc, "oracle"), None),
+        "p273_alt_w100_sel": (MG.std_spec(273, alt(300), 32, sel, "oracle"), None),
+        "p52_tree_default": (MG.std_spec(52, ((G, 200), (P, 200), (G, 200)), 33, conc,
+                                         "tree:x"), "tree52"),
+    }
+
+
+def main(argv):
+    todo = loops()
+    ids = argv or list(todo)
+    npz, js = OUT / "loops_long.npz", OUT / "loops_long.json"
+    arr = dict(np.load(npz)) if npz.exists() else {}
+    meta = {m["id"]: m for m in json.loads(js.read_text())["loops"]} if js.exists() else {}
+    trees = {"tree52": SP.from_text((OUT / "tree_52prb.txt").read_text())}
+    for lid in ids:
+        spec, tname = todo[lid]
+        m, recs, extra = MG.run_loop(spec, trees.get(tname), tname)
+        m["id"] = lid
+        meta[lid] = m
+        arr[f"{lid}__records"] = recs
+        arr[f"{lid}__extra"] = extra
+        print("loop", lid, "slots", len(m["modes"]), "mode changes",
+              sum(a != b for a, b in zip(m["modes"], m["modes"][1:])),
+              "msgs", len(m["messages"]), flush=True)
+        np.savez_compressed(npz, **arr)
+        js.write_text(json.dumps({"versions": MG.versions(), "loops": list(meta.values())},
+                                 indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
