@@ -45,6 +45,14 @@ def loops():
     return [(m, arrs[m["id"] + "__records"], arrs[m["id"] + "__extra"]) for m in meta]
 
 
+@functools.lru_cache(maxsize=None)
+def loops_long():
+    """Long loops at the benched shapes (tools/make_golden_long.py)."""
+    meta = json.loads((GOLDEN / "loops_long.json").read_text())["loops"]
+    arrs = np.load(GOLDEN / "loops_long.npz")
+    return [(m, arrs[m["id"] + "__records"], arrs[m["id"] + "__extra"]) for m in meta]
+
+
 def loop_case(lid):
     for m, r, e in loops():
         if m["id"] == lid:

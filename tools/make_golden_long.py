@@ -11,7 +11,7 @@ These pin the BENCHED shapes themselves (VERDICT r1 "next" item 1):
                          chunk boundary and the bench's 256-slot batch boundary)
   p273_alt_w100_sel   -- the same in selected-only mode, 300 slots
   p52_tree_default    -- config A: 52 PRB, 4 RX, tree policy with the DEFAULT dApp
-                         (decision period 100, window 100), 600 slots G/P/G
+                         (decision period 100, window 100), 600 slots P/G/P (decisions 0,0,0,0,1,0)
 Recorded: KPM rows (KpmRecord.row(), phy_pipeline.py:291-310), per-slot
 post-eq SINR / |H| mean / CRC, modes, control messages, fail-safe events
 (harness.execute_run, harness.py:174-231).
@@ -39,7 +39,7 @@ def loops():
     return {
         "p273_alt_w100_conc": (MG.std_spec(273, alt(320), 31, conc, "oracle"), None),
         "p273_alt_w100_sel": (MG.std_spec(273, alt(300), 32, sel, "oracle"), None),
-        "p52_tree_default": (MG.std_spec(52, ((G, 200), (P, 200), (G, 200)), 33, conc,
+        "p52_tree_default": (MG.std_spec(52, ((P, 200), (G, 200), (P, 200)), 33, conc,
                                          "tree:x"), "tree52"),
     }
 
