@@ -285,7 +285,10 @@ int arches_ls_materialize(const arches_plan* plan, int32_t n_units, const void* 
                           const void* pilots, void* ls, arches_stream_t stream);
 /* estimate_noise_var / mmse_estimate / denoiser_estimate from an LS grid
  * ls[u][A][D][N]; which: 0 = noise var only, 1 = MMSE (noise_var_in[u] >= 0
- * overrides sigma2_hat), 2 = denoiser (general N-point analysis) */
+ * overrides sigma2_hat), 2 = denoiser (general N-point analysis); OR-ing
+ * ARCHES_EXPERT_OUT_C128 makes `out` complex128 (fp64 synthesis, the
+ * reference's output dtype) instead of complex64 */
+#define ARCHES_EXPERT_OUT_C128 0x100
 int arches_expert_from_ls(const arches_plan* plan, int32_t n_units, int32_t which,
                           const void* ls, const double* noise_var_in, double* sigma2_hat,
                           void* out, void* ws, arches_stream_t stream);

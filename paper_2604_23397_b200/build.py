@@ -5,6 +5,7 @@ by `__graft_entry__.build()` and by `python -m paper_2604_23397_b200.build`.
 """
 from __future__ import annotations
 
+import hashlib
 import os
 import pathlib
 import shutil
@@ -15,7 +16,10 @@ PKG = pathlib.Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "lib" / "libarches.so"
+STAMP = LIB.with_name("libarches.so.sha256")   # digest of the sources + flags it was built from
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC", "-Xcompiler",
+         "-fvisibility=default", "-cudart", "static"]
 
 
 def nvcc() -> str:
@@ -29,11 +33,21 @@ def sources():
     return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "arches.h"]
 
 
+def source_digest() -> str:
+    h = hashlib.sha256()
+    h.update(" ".join(ARCH + FLAGS).encode())
+    for p in sources():
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
-    if not LIB.exists():
+    """Rebuild unless the library exists AND was built from exactly these sources
+    (a content hash, not mtimes: a copied-in stale .so with a newer mtime is rebuilt)."""
+    if not LIB.exists() or not STAMP.exists():
         return True
-    t = LIB.stat().st_mtime
-    return any(p.stat().st_mtime > t for p in sources())
+    return STAMP.read_text().strip() != source_digest()
 
 
 def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
@@ -41,8 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
         return LIB
     LIB.parent.mkdir(parents=True, exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=default", "-cudart", "static", "-I", str(ROOT / "include"),
+    cmd = [nvcc(), *ARCH, *FLAGS, "-I", str(ROOT / "include"),
            "-Xptxas", "-v" if verbose else "-O3", str(CSRC / "arches.cu"), "-o", str(tmp)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -51,6 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(tmp, LIB)
+    STAMP.write_text(source_digest() + "\n")
     return LIB
 
 

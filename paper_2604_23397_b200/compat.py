@@ -99,7 +99,7 @@ def _dev_ls(values: np.ndarray):
 
 
 def _host_est(dev) -> np.ndarray:
-    """device (1, A, D, N) complex64 -> (A, 1, N, D) complex128."""
+    """device (1, A, D, N) complex -> (A, 1, N, D) complex128."""
     arr = dev[0].cpu().numpy()
     return np.ascontiguousarray(np.transpose(arr, (0, 2, 1))[:, None, :, :]).astype(np.complex128)
 
@@ -167,9 +167,10 @@ def mmse_estimate(ls, noise_var: float, scenario, block_prbs: int = 32):
     geo = ls.geometry
     ent = _plan(geo, block_prbs=block_prbs, ds=float(scenario.assumed_delay_spread))
     nv = torch.tensor([float(noise_var)], dtype=torch.float64, device="cuda")
-    out = torch.empty((1, geo.n_ant, len(geo.dmrs_symbols), geo.n_sc), dtype=torch.complex64,
-                      device="cuda")
-    _check(_lib.lib().arches_expert_from_ls(ent.plan.handle, 1, 1, _lib.ptr(_dev_ls(ls.values)),
+    out = torch.empty((1, geo.n_ant, len(geo.dmrs_symbols), geo.n_sc), dtype=torch.complex128,
+                      device="cuda")   # fp64 synthesis: the reference's output dtype
+    _check(_lib.lib().arches_expert_from_ls(ent.plan.handle, 1, 1 | _lib.EXPERT_OUT_C128,
+                                            _lib.ptr(_dev_ls(ls.values)),
                                             _lib.ptr(nv), None, _lib.ptr(out), _lib.ptr(ent.ws),
                                             _stream()))
     return _estimate(_host_est(out), "Interpolated", np.ones(geo.n_sc, dtype=bool), geo, like=ls)
@@ -182,8 +183,9 @@ def denoiser_estimate(ls, geometry, truncation: int = 20):
     torch = _torch()
     ent = _plan(geometry, truncation=truncation)
     out = torch.empty((1, geometry.n_ant, len(geometry.dmrs_symbols), geometry.n_sc),
-                      dtype=torch.complex64, device="cuda")
-    _check(_lib.lib().arches_expert_from_ls(ent.plan.handle, 1, 2, _lib.ptr(_dev_ls(ls.values)),
+                      dtype=torch.complex128, device="cuda")   # fp64 synthesis
+    _check(_lib.lib().arches_expert_from_ls(ent.plan.handle, 1, 2 | _lib.EXPERT_OUT_C128,
+                                            _lib.ptr(_dev_ls(ls.values)),
                                             None, None, _lib.ptr(out), _lib.ptr(ent.ws),
                                             _stream()))
     return _estimate(_host_est(out), "Interpolated", np.ones(geometry.n_sc, dtype=bool),
@@ -215,18 +217,19 @@ def equalize(rx, estimate, noise_var: float, tx_grid, sinr_cap_db: float = 60.0)
 # ---------------------------------------------------------- switch plumbing
 
 class DeviceArray:
-    """A device-resident complex buffer that numpy can read (`__array__` copies
-    device -> host, complex128 like the reference buffers)."""
+    """A device-resident complex128 buffer (the reference buffers' dtype, so a
+    written expert output reads back element-exact) that numpy can read
+    (`__array__` copies device -> host)."""
 
     def __init__(self, shape):
         torch = _torch()
         self.shape = tuple(shape)
-        self.tensor = torch.zeros(self.shape, dtype=torch.complex64, device="cuda")
+        self.tensor = torch.zeros(self.shape, dtype=torch.complex128, device="cuda")
 
     dtype = np.dtype(np.complex128)
 
     def __array__(self, dtype=None, copy=None):
-        a = self.tensor.cpu().numpy().astype(np.complex128)
+        a = self.tensor.cpu().numpy()
         return a if dtype is None else a.astype(dtype)
 
     def __len__(self):
@@ -240,7 +243,7 @@ class DeviceArray:
         if isinstance(values, DeviceArray):
             src = values.tensor
         else:
-            src = torch.from_numpy(np.asarray(values, dtype=np.complex64)).to("cuda")
+            src = torch.from_numpy(np.asarray(values, dtype=np.complex128)).to("cuda")
         self.tensor[idx] = src
 
 
@@ -282,8 +285,9 @@ def switch_select(buffers, mode, costs) -> float:
         torch = _torch()
         flag = torch.tensor([1], dtype=torch.int32, device="cuda")
         src, dst = buffers.buffer_mmse.tensor, buffers.buffer_ai.tensor
+        # complex128 buffers: 2 interleaved float2 per element
         _check(_lib.lib().arches_switch_copy_one(_lib.ptr(flag), _lib.ptr(src), _lib.ptr(dst),
-                                                 src.numel(), _stream()))
+                                                 2 * src.numel(), _stream()))
     elif not buffers.populated(0):
         raise _E.PipelineStateError("AI buffer unpopulated at switch_select")
     return costs.switch_cost_us(m)

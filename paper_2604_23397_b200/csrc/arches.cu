@@ -1063,6 +1063,8 @@ extern "C" int arches_ls_materialize(const arches_plan* plan, int32_t n_units, c
 extern "C" int arches_expert_from_ls(const arches_plan* plan, int32_t n_units, int32_t which,
                                      const void* ls, const double* noise_var_in, double* sigma2_hat,
                                      void* out, void* ws, arches_stream_t stream) {
+  const bool c128 = (which & ARCHES_EXPERT_OUT_C128) != 0;
+  which &= ~ARCHES_EXPERT_OUT_C128;
   if (!plan || !ls || !ws || n_units < 1 || which < 0 || which > 2)
     return set_err(ARCHES_E_CONTRACT, "bad expert_from_ls args");
   if ((which == 1 || which == 2) && !out) return set_err(ARCHES_E_CONTRACT, "missing output");
@@ -1086,8 +1088,12 @@ extern "C" int arches_expert_from_ls(const arches_plan* plan, int32_t n_units, i
   }
   if (rc || which == 0) return rc;
   dim3 grid((plan->dev.N + 127) / 128, n_units);
-  k_synth_one<<<grid, 128, 0, s>>>(plan->dev, ws_at<float2>(ws, w.coef), which,
-                                   reinterpret_cast<float2*>(out));
+  if (c128)
+    k_synth_one_f64<<<grid, 128, 0, s>>>(plan->dev, ws_at<float2>(ws, w.coef), which,
+                                         reinterpret_cast<double2*>(out));
+  else
+    k_synth_one<<<grid, 128, 0, s>>>(plan->dev, ws_at<float2>(ws, w.coef), which,
+                                     reinterpret_cast<float2*>(out));
   LAUNCH_CHECK();
   return ARCHES_OK;
 }

@@ -376,3 +376,31 @@ __global__ void k_synth_one(const PlanDev P, const float2* coef, int which /*1 m
     out[((size_t)u * AD + ad) * P.N + k] = acc;
   }
 }
+
+// Per-call compat form with complex128 output: the same taps synthesised in
+// fp64 (fp64 twiddles from sincospi), so the output is band-limited to the
+// reference's fp64 rounding -- e.g. ifft of the denoiser output vanishes
+// beyond the truncation to ~1e-16 (test_expert_bank.py:103-114 asserts 1e-12).
+__global__ void k_synth_one_f64(const PlanDev P, const float2* coef, int which, double2* out) {
+  const int u = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P.N) return;
+  const int AD = P.A * P.D;
+  const float2* cm = coef + (size_t)u * coef_floats2(P);
+  const float2* ca = cm + (size_t)AD * P.n_blocks * 8;
+  const int b = min(k / P.block, P.n_blocks - 1);
+  const int kl = (which == 1) ? k - b * P.block : k;
+  const int nt = (which == 1) ? 8 : P.trunc;
+  for (int ad = 0; ad < AD; ++ad) {
+    double re = 0.0, im = 0.0;
+    for (int l = 0; l < nt; ++l) {
+      const float2 c = (which == 1) ? cm[((size_t)ad * P.n_blocks + b) * 8 + l] : ca[ad * P.trunc + l];
+      double sn, cs;
+      sincospi(2.0 * (double)(((long long)l * kl) % P.N) / (double)P.N, &sn, &cs);
+      // c * e^{-i theta}
+      re = fma((double)c.x, cs, fma((double)c.y, sn, re));
+      im = fma((double)c.y, cs, fma(-(double)c.x, sn, im));
+    }
+    out[((size_t)u * AD + ad) * P.N + k] = make_double2(re, im);
+  }
+}
