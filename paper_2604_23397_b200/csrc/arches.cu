@@ -1031,8 +1031,9 @@ extern "C" int arches_switch_copy(const arches_plan* plan, int32_t n_units, cons
   if (per_unit % 2) return set_err(ARCHES_E_CONTRACT, "unit size must be even");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const size_t f4 = per_unit / 2;
-  dim3 grid((unsigned)std::min<size_t>((f4 + 255) / 256, 64), n_units);
-  k5_switch_copy<<<grid, 256, 0, s>>>(kpm, reinterpret_cast<const float4*>(h_mmse),
+  const size_t blocks = std::min<size_t>((f4 * (size_t)n_units + 255) / 256,
+                                         (size_t)plan->dev.num_sms * 16);
+  k5_switch_copy<<<(unsigned)std::max<size_t>(blocks, 1), 256, 0, s>>>(kpm, reinterpret_cast<const float4*>(h_mmse),
                                       reinterpret_cast<float4*>(h_ai), f4, n_units);
   LAUNCH_CHECK();
   return ARCHES_OK;

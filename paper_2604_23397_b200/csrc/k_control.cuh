@@ -225,16 +225,16 @@ __global__ void k4_state_init(const PlanDev P, void* state, int n_streams) {
   *sv.h = st;
 }
 
-// K5: mode-predicated coalesced copy of the MMSE output into the AI buffer
+// K5: mode-predicated coalesced copy of the MMSE output into the AI buffer;
+// grid-stride over every (unit, float4) of the batch (any number of units)
 __global__ void k5_switch_copy(const arches_kpm* kpm, const float4* src, float4* dst,
                                size_t per_unit_f4, int n_units) {
-  const int u = blockIdx.y;
-  if (u >= n_units || kpm[u].mode != 1) return;  // mode 0: no-op
-  const float4* s = src + (size_t)u * per_unit_f4;
-  float4* d = dst + (size_t)u * per_unit_f4;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < per_unit_f4;
-       i += (size_t)gridDim.x * blockDim.x)
-    d[i] = s[i];
+  const size_t total = per_unit_f4 * (size_t)n_units;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t u = i / per_unit_f4;
+    if (__ldg(&kpm[u].mode) == 1) dst[i] = src[i];  // mode 0: no-op
+  }
 }
 
 __global__ void k5_switch_copy_one(const int32_t* mode, const float2* src, float2* dst, size_t n) {

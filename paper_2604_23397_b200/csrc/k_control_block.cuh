@@ -19,6 +19,7 @@
 #include "k_control_warp.cuh"
 
 #define K4B_THREADS 256
+#define K4B_WIN_ROWS 128  // dApp window rows staged per pass (10 KB of fp64)
 
 // block-wide inclusive scan (blockDim == K4B_THREADS); `tmp` holds one entry per warp
 template <typename T>
@@ -48,6 +49,7 @@ __global__ void __launch_bounds__(K4B_THREADS) k4_kpm_scan_block(const PlanDev P
   __shared__ int s_len, s_decide;
   __shared__ StreamState s_st;
   __shared__ double s_feat[ARCHES_FEATURES];
+  __shared__ double s_win[K4B_WIN_ROWS * ARCHES_FEATURES];
   StateView sv = state_view(a.state, stream, P.window_length, P.dapp_window);
   if (tid == 0) s_st = *sv.h;
   __syncthreads();
@@ -290,14 +292,22 @@ __global__ void __launch_bounds__(K4B_THREADS) k4_kpm_scan_block(const PlanDev P
     if (decide) {
       const int64_t nd = n0 + len - 1;
       const int rows = (int)min((long long)WD, (long long)nd + 1);
-      if (tid < ARCHES_FEATURES) {
-        double acc = 0.0;
-        for (int i = 0; i < rows; ++i) {
-          const int64_t p = nd - rows + 1 + i;  // oldest first
-          acc = xadd(acc, sv.feat[(size_t)(p % WD) * ARCHES_FEATURES + tid]);
+      // the window rows are staged into shared memory by the whole CTA (coalesced,
+      // all loads in flight at once), then threads 0..9 add them in slot order
+      double acc = 0.0;
+      for (int r0 = 0; r0 < rows; r0 += K4B_WIN_ROWS) {
+        const int nr = min(K4B_WIN_ROWS, rows - r0);
+        for (int i = tid; i < nr * ARCHES_FEATURES; i += K4B_THREADS) {
+          const int r = i / ARCHES_FEATURES, f = i - r * ARCHES_FEATURES;
+          const int64_t p = nd - rows + 1 + r0 + r;  // oldest first
+          s_win[i] = sv.feat[(size_t)(p % WD) * ARCHES_FEATURES + f];
         }
-        s_feat[tid] = xdiv(acc, (double)rows);
+        __syncthreads();
+        if (tid < ARCHES_FEATURES)
+          for (int r = 0; r < nr; ++r) acc = xadd(acc, s_win[r * ARCHES_FEATURES + tid]);
+        __syncthreads();
       }
+      if (tid < ARCHES_FEATURES) s_feat[tid] = xdiv(acc, (double)rows);
       __syncthreads();
       if (tid == 0) {
         StreamState& st = s_st;
