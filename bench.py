@@ -331,6 +331,7 @@ def run_ours(a, rank, world, backend):
     from paper_2604_23397_b200.dist import reduce_metrics
     from paper_2604_23397_b200.engine import ArchesPlan, SlotEngine
     from paper_2604_23397_b200.policy import from_text
+    from paper_2604_23397_b200.scene import pack_qpsk
 
     dev = torch.device("cuda", torch.cuda.current_device())
     red_dev = dev if backend == "nccl" else None
@@ -421,7 +422,9 @@ def run_ours(a, rank, world, backend):
     k1 = np.mean([ev[4 * r].elapsed_time(ev[4 * r + 1]) for r in range(reps)])
     k2 = np.mean([ev[4 * r + 1].elapsed_time(ev[4 * r + 2]) for r in range(reps)])
     k4 = np.mean([ev[4 * r + 2].elapsed_time(ev[4 * r + 3]) for r in range(reps)])
-    unit_bytes = 8 * N * (20 * A + 14)          # y + tx read once, both experts written
+    # algorithmic bytes per unit: y read once (8 A T N), both experts written
+    # (2 x 8 A D N), the complex64 genie tx read once (8 T N) = 8 N (20 A + 14)
+    unit_bytes = 8 * N * (A * (T + 2 * D) + T)
     pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(pk_path)) if os.path.exists(pk_path) else {"hbm_gbs": 6650.0}
     peak = float(peaks["hbm_gbs"])
@@ -443,7 +446,10 @@ def run_ours(a, rank, world, backend):
     # bound to it), as a PHY host process would run; affinity restored after.
     aff0 = gpu_numa_bind(torch.cuda.current_device())
     y_h = torch.from_numpy(y).pin_memory()
-    tx_h = torch.from_numpy(tx).pin_memory()
+    # the transmit grids cross PCIe in the packed QPSK wire format (2 bits per RE,
+    # expanded on the device by arches_unpack_qpsk inside load())
+    tx_host = pack_qpsk(tx)
+    tx_h = torch.from_numpy(tx_host).pin_memory()
     nv_h = torch.from_numpy(nv).pin_memory()
     reg_h = torch.from_numpy(reg).pin_memory()
     kpm_h = torch.empty(eng.kpm.numel(), dtype=torch.uint8).pin_memory()
@@ -463,7 +469,7 @@ def run_ours(a, rank, world, backend):
     te, e2e_units = reduce_metrics(e2.elapsed_time(e3), K * U, red_dev)
     recs = kpm_h.numpy().view(_lib.KPM_DTYPE)
     assert recs["slot_index"][-1] > 0 and set(np.unique(recs["mode"])) <= {0, 1}
-    h2d = y.nbytes + tx.nbytes + nv.nbytes + reg.nbytes
+    h2d = y.nbytes + tx_host.nbytes + nv.nbytes + reg.nbytes
     d2h = kpm_h.numel()
     if aff0 is not None:
         os.sched_setaffinity(0, aff0)
@@ -493,6 +499,26 @@ def run_ours(a, rank, world, backend):
                "max_us": float(us.max()), "slots": int(len(us)),
                "how": "1 slot of one stream per CUDA-graph launch (K1, K1 finalize, K2, K3, K4), "
                       "CUDA events, inputs in HBM"}
+        # host-to-host: the slot's pinned y + packed tx -> H2D -> unpack + graph ->
+        # D2H KPM record -> host holds the decision (wall clock, one slot at a time)
+        y1 = [torch.from_numpy(y[j:j + 1]).pin_memory() for j in range(min(S, 16))]
+        t1 = [torch.from_numpy(pack_qpsk(tx[j:j + 1])).pin_memory() for j in range(min(S, 16))]
+        k1h = torch.empty(eng1.kpm.numel(), dtype=torch.uint8).pin_memory()
+        h2h = []
+        for i in range(a.latency_slots):
+            j = i % len(y1)
+            t0 = time.perf_counter()
+            eng1.load(y=y1[j], tx=t1[j], non_blocking=True)
+            eng1.run()
+            k1h.copy_(eng1.kpm, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            h2h.append((time.perf_counter() - t0) * 1e6)
+        h2h = np.array(h2h[5:])
+        lat["host_to_host"] = {
+            "p50_us": float(np.percentile(h2h, 50)), "p99_us": float(np.percentile(h2h, 99)),
+            "max_us": float(h2h.max()), "slots": int(len(h2h)),
+            "how": "wall clock per slot: pinned y (1 slot, complex64) + packed tx -> H2D -> "
+                   "unpack + CUDA-graph step -> D2H KPM record -> stream sync"}
 
     line = None
     if rank == 0:
@@ -528,8 +554,9 @@ def run_ours(a, rank, world, backend):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_units / (te / 1000.0), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "how": "pinned host y/tx/noise_var/regime -> H2D -> run (graph) -> D2H KPM "
-                           "records, every step, one stream"},
+                    "how": "pinned host y (complex64) + tx (packed QPSK wire format, 2 bits/RE) + "
+                           "noise_var + regime -> H2D -> unpack + run (graph) -> D2H KPM records, "
+                           "every step, one stream"},
             "latency": lat,
             "gpu_launches": 6 * K,  # RNG, K1, K1 finalize, K2, K3, K4 per step
             "clocks": clk,

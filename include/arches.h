@@ -279,6 +279,24 @@ int arches_switch_copy(const arches_plan* plan, int32_t n_units, const arches_kp
 int arches_switch_copy_one(const int32_t* mode, const void* src, void* dst, size_t n,
                            arches_stream_t stream);
 
+/* ---- packed QPSK transmit grids (host <-> device wire format) -------
+ * The genie transmit grid the equaliser scores against is QPSK everywhere
+ * (qpsk(), rng.py:50-55, pilots included: radio_scene.py:240-249), so it
+ * crosses PCIe as 2-bit codes: tx_bits[u][n_tiles][T][32] bytes, n_tiles =
+ * ceil(N / 128); the RE (symbol t, subcarrier k = 128 tile + j) is byte j / 4
+ * of row t, bits 2 (j % 4) .. +1: bit 0 set = Re > 0, bit 1 set = Im > 0, value
+ * ((2 b0 - 1) + i (2 b1 - 1)) * float(1/sqrt(2)) -- exactly the complex64 of
+ * qpsk().  Pad codes (k >= N) are ignored.  K2 reads the complex64 grid
+ * (decoding 2-bit codes in its issue-bound epilogue measured slower than the
+ * 94 MB per 256 slots it would save), so unpack once per batch after the H2D.
+ * arches_pack_qpsk sets *bad (device int, caller-zeroed) to 1 when any RE is
+ * not exactly a qpsk() symbol. */
+size_t arches_tx_bits_bytes(const arches_plan* plan, int32_t n_units);
+int arches_pack_qpsk(const arches_plan* plan, int32_t n_units, const void* tx, void* tx_bits,
+                     int32_t* bad, arches_stream_t stream);
+int arches_unpack_qpsk(const arches_plan* plan, int32_t n_units, const void* tx_bits, void* tx,
+                       arches_stream_t stream);
+
 /* ---- per-call drop-in forms (compat layer) -------------------------- */
 /* ls_estimate: materialise the comb-filled LS grid ls[u][A][D][N] */
 int arches_ls_materialize(const arches_plan* plan, int32_t n_units, const void* y,

@@ -91,6 +91,9 @@ _SIGS = {
     "arches_ls_materialize": (C.c_int, [P, C.c_int32, P, P, P, P]),
     "arches_expert_from_ls": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, P, P, P]),
     "arches_equalize": (C.c_int, [P, C.c_int32, P, P, P, P, P, P, P, P, P, P]),
+    "arches_pack_qpsk": (C.c_int, [P, C.c_int32, P, P, P, P]),
+    "arches_tx_bits_bytes": (C.c_size_t, [P, C.c_int32]),
+    "arches_unpack_qpsk": (C.c_int, [P, C.c_int32, P, P, P]),
     "arches_window_features": (C.c_int, [P, C.c_int32, P, P]),
     "arches_tree_predict": (C.c_int, [P, P, C.c_int32, C.c_int32, P, P]),
     "arches_last_error": (C.c_char_p, []),

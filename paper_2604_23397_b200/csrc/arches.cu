@@ -1050,6 +1050,41 @@ extern "C" int arches_switch_copy_one(const int32_t* mode, const void* src, void
   return ARCHES_OK;
 }
 
+// ------------------------------------------------------------ packed QPSK tx
+extern "C" size_t arches_tx_bits_bytes(const arches_plan* plan, int32_t n_units) {
+  if (!plan || n_units < 1) return 0;
+  return (size_t)n_units * plan->dev.n_tiles * plan->dev.T * ARCHES_TXB_ROW;
+}
+
+static unsigned qpsk_blocks(const arches_plan* plan, size_t n_bytes) {
+  return (unsigned)std::max<size_t>(1, std::min<size_t>((n_bytes + 255) / 256,
+                                                        (size_t)plan->dev.num_sms * 8));
+}
+
+extern "C" int arches_pack_qpsk(const arches_plan* plan, int32_t n_units, const void* tx,
+                                void* tx_bits, int32_t* bad, arches_stream_t stream) {
+  if (!plan || !tx || !tx_bits || !bad || n_units < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad pack_qpsk args");
+  const size_t n_bytes = arches_tx_bits_bytes(plan, n_units);
+  k_pack_qpsk<<<qpsk_blocks(plan, n_bytes), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      plan->dev, reinterpret_cast<const float2*>(tx), reinterpret_cast<unsigned char*>(tx_bits),
+      bad, n_bytes);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_unpack_qpsk(const arches_plan* plan, int32_t n_units, const void* tx_bits,
+                                  void* tx, arches_stream_t stream) {
+  if (!plan || !tx || !tx_bits || n_units < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad unpack_qpsk args");
+  const size_t n_bytes = arches_tx_bits_bytes(plan, n_units);
+  k_unpack_qpsk<<<qpsk_blocks(plan, n_bytes), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      plan->dev, reinterpret_cast<const unsigned char*>(tx_bits), reinterpret_cast<float2*>(tx),
+      n_bytes);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
 // ------------------------------------------------------------ compat forms
 extern "C" int arches_ls_materialize(const arches_plan* plan, int32_t n_units, const void* y,
                                      const void* pilots, void* ls, arches_stream_t stream) {

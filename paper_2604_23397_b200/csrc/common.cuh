@@ -11,6 +11,8 @@
 #define ARCHES_RL 5            // K1 register tile: delay bins per thread
 #define ARCHES_MAX_AD (ARCHES_MAX_ANT * ARCHES_MAX_DMRS)
 #define ARCHES_FEATURES 10
+#define ARCHES_QPSK_AMP 0x3F3504F3u  // float(1/sqrt(2)): the complex64 of qpsk() (rng.py:50-55)
+#define ARCHES_TXB_ROW 32            // packed tx bytes per (tile, symbol): 128 REs x 2 bits
 
 // Plan constants passed by value to every kernel (tables live in device memory).
 struct PlanDev {

@@ -258,3 +258,53 @@ __global__ void k_tree_predict(const arches_tree* tree, const double* x, int n, 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) labels[i] = tree_descend(tree, x + (size_t)i * nf);
 }
+
+// tx[u][T][N] complex64 -> packed QPSK codes [u][n_tiles][T][32] (ARCHES_FLAG_TX_QPSK2);
+// one thread per code byte (4 REs); any RE that is not exactly a qpsk() symbol
+// raises *bad
+__global__ void k_pack_qpsk(const PlanDev P, const float2* tx, unsigned char* bits, int32_t* bad,
+                            size_t n_bytes) {
+  const float q = __uint_as_float(ARCHES_QPSK_AMP);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bytes;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = i / ARCHES_TXB_ROW;  // (u, tile, t)
+    const int jb = (int)(i - row * ARCHES_TXB_ROW);
+    const int t = (int)(row % P.T);
+    const size_t ut = row / P.T;
+    const int tile = (int)(ut % P.n_tiles);
+    const size_t u = ut / P.n_tiles;
+    unsigned int code = 0;
+    bool ok = true;
+    for (int r = 0; r < 4; ++r) {
+      const int k = tile * ARCHES_TILE + jb * 4 + r;
+      if (k >= P.N) break;
+      const float2 x = tx[(u * P.T + t) * (size_t)P.N + k];
+      ok = ok && (x.x == q || x.x == -q) && (x.y == q || x.y == -q);
+      code |= ((x.x > 0.f ? 1u : 0u) | (x.y > 0.f ? 2u : 0u)) << (2 * r);
+    }
+    bits[i] = (unsigned char)code;
+    if (!ok) *bad = 1;
+  }
+}
+
+// packed QPSK codes -> the complex64 grid tx[u][T][N]; one thread per code byte
+__global__ void k_unpack_qpsk(const PlanDev P, const unsigned char* bits, float2* tx, size_t n_bytes) {
+  const float q = __uint_as_float(ARCHES_QPSK_AMP);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bytes;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = i / ARCHES_TXB_ROW;  // (u, tile, t)
+    const int jb = (int)(i - row * ARCHES_TXB_ROW);
+    const int t = (int)(row % P.T);
+    const size_t ut = row / P.T;
+    const int tile = (int)(ut % P.n_tiles);
+    const size_t u = ut / P.n_tiles;
+    const unsigned int code = bits[i];
+    float2* dst = tx + (u * P.T + t) * (size_t)P.N;
+    for (int r = 0; r < 4; ++r) {
+      const int k = tile * ARCHES_TILE + jb * 4 + r;
+      if (k >= P.N) break;
+      const unsigned int c = code >> (2 * r);
+      dst[k] = make_float2((c & 1u) ? q : -q, (c & 2u) ? q : -q);
+    }
+  }
+}

@@ -193,8 +193,10 @@ class SlotEngine:
 
     def load(self, y=None, tx=None, noise_var=None, regime=None, non_blocking=False):
         """Copy one batch of inputs (host or device tensors / numpy) into the engine.
-        y: (U, A, T, N) complex64 device layout; tx: (U, T, N); noise_var: (U,);
-        regime: (U,) 1 = good."""
+        y: (U, A, T, N) complex64 device layout; tx: (U, T, N) complex grid, or the
+        packed QPSK wire format (U, n_tiles, T, 32) uint8 (scene.pack_qpsk: 2 bits
+        per RE over PCIe, expanded on the device by arches_unpack_qpsk);
+        noise_var: (U,); regime: (U,) 1 = good."""
         import torch
         self._settle()   # K4(n-1) may still read regime / noise_var
 
@@ -207,9 +209,38 @@ class SlotEngine:
             dst.copy_(t, non_blocking=non_blocking)
 
         put(self.y, y, np.complex64)
-        put(self.tx, tx, np.complex64)
+        if tx is not None and (tx.dtype == torch.uint8 if isinstance(tx, torch.Tensor)
+                               else np.asarray(tx).dtype == np.uint8):
+            self._load_tx_bits(tx, non_blocking)
+        else:
+            put(self.tx, tx, np.complex64)
         put(self.noise_var, noise_var, np.float64)
         put(self.regime, regime, np.int8)
+
+    def _load_tx_bits(self, bits, non_blocking):
+        import torch
+        shape = (self.U, -(-self.N // 128), self.T, 32)
+        t = bits if isinstance(bits, torch.Tensor) else torch.from_numpy(np.asarray(bits))
+        if tuple(t.shape) != shape:
+            raise ContractViolation(f"packed tx shape {tuple(t.shape)}, expected {shape}")
+        if getattr(self, "_tx_bits", None) is None:
+            self._tx_bits = torch.empty(shape, dtype=torch.uint8, device=self.device)
+        self._tx_bits.copy_(t, non_blocking=non_blocking)
+        _lib.check(_lib.lib().arches_unpack_qpsk(self.plan.handle, self.U, _lib.ptr(self._tx_bits),
+                                                 _lib.ptr(self.tx), _stream_handle()))
+
+    def pack_tx(self) -> np.ndarray:
+        """The loaded transmit grids in the packed QPSK wire format (device packer;
+        ContractViolation if any RE is not a qpsk() symbol)."""
+        import torch
+        out = torch.empty((self.U, -(-self.N // 128), self.T, 32), dtype=torch.uint8,
+                          device=self.device)
+        bad = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _lib.check(_lib.lib().arches_pack_qpsk(self.plan.handle, self.U, _lib.ptr(self.tx),
+                                               _lib.ptr(out), _lib.ptr(bad), _stream_handle()))
+        if int(bad.item()):
+            raise ContractViolation("tx grid is not QPSK (+-1 +-1j)/sqrt(2) in complex64")
+        return out.cpu().numpy()
 
     # ------------------------------------------------------------ run
     def _launch(self, first_slot: int, pipelined: bool = False):

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import ConfigurationError
+from .errors import ConfigurationError, ContractViolation
 from .geometry import GOOD, N_TAPS, ScenarioConfig, SlotGeometry, pdp_powers
 
 _U64 = (1 << 64) - 1
@@ -177,3 +177,30 @@ def lcid4_jitter(slot: int) -> float:
     """Seed-independent traffic wobble in [-1, 1) (`phy_pipeline.py:347-350`)."""
     d = hashlib.blake2b(f"lcid4:{slot}".encode(), digest_size=8).digest()
     return int.from_bytes(d, "little") / float(1 << 64) * 2.0 - 1.0
+
+
+QPSK_AMP = np.float32(1.0 / np.sqrt(2.0))   # the complex64 of qpsk() (rng.py:50-55)
+TX_TILE, TX_ROW_BYTES = 128, 32
+
+
+def pack_qpsk(tx: np.ndarray) -> np.ndarray:
+    """Transmit grids (U, T, N) complex -> packed QPSK codes (U, n_tiles, T, 32) uint8,
+    the packed wire format of include/arches.h (arches_unpack_qpsk): RE (t, 128 * tile + j) is
+    byte j // 4 of row t, bits 2 (j % 4): bit 0 = Re > 0, bit 1 = Im > 0.  Every RE
+    must be exactly a qpsk() symbol in complex64 (the whole grid is QPSK, pilots
+    included: radio_scene.py:240-249)."""
+    x = np.asarray(tx)
+    if x.ndim != 3:
+        raise ContractViolation(f"tx shape {x.shape}, expected (units, n_sym, n_sc)")
+    x = x.astype(np.complex64, copy=False)
+    re, im = x.real, x.imag
+    if not (np.all(np.abs(re) == QPSK_AMP) and np.all(np.abs(im) == QPSK_AMP)):
+        raise ContractViolation("tx grid is not QPSK (+-1 +-1j)/sqrt(2) in complex64: "
+                                "load it as a complex grid")
+    U, T, N = x.shape
+    n_tiles = -(-N // TX_TILE)
+    code = np.zeros((U, T, n_tiles * TX_TILE), np.uint8)
+    code[:, :, :N] = (re > 0).astype(np.uint8) | ((im > 0).astype(np.uint8) << 1)
+    q = code.reshape(U, T, n_tiles, TX_ROW_BYTES, 4)
+    packed = q[..., 0] | (q[..., 1] << 2) | (q[..., 2] << 4) | (q[..., 3] << 6)
+    return np.ascontiguousarray(packed.transpose(0, 2, 1, 3))   # (U, n_tiles, T, 32)
