@@ -279,6 +279,36 @@ int arches_switch_copy(const arches_plan* plan, int32_t n_units, const arches_kp
 int arches_switch_copy_one(const int32_t* mode, const void* src, void* dst, size_t n,
                            arches_stream_t stream);
 
+/* ---- downstream of the switch (after K4 fixed each slot's mode) ------
+ * K6: x_hat of the SELECTED expert per unit (kpm.mode: 1 = h_mmse, 0 = h_ai --
+ * the buffer switch_select leaves downstream), formed exactly like equalize()
+ * (phy_pipeline.py:258-266: time interpolation, MRC num / (sum |h|^2 +
+ * noise_var), every RE): x_hat[u][T][N] complex64 (NULL = skip); and max-log
+ * LLRs log P(b=0)/P(b=1) for the slot's scheduled modulation (kpm.qam_order:
+ * Gray QPSK / 16QAM / 64QAM, TS 38.211 s5.1.3-5.1.5) of the unbiased symbol
+ * x_hat / beta, beta = den / (den + noise_var), noise variance noise_var / den:
+ * llr[u][T][N][ARCHES_LLR_STRIDE] floats, bit i of the RE at [i], zero on pilot
+ * REs and beyond qam_order (NULL = skip). */
+#define ARCHES_LLR_STRIDE 6
+int arches_downstream(const arches_plan* plan, int32_t n_units, const arches_kpm* kpm,
+                      const void* h_mmse, const void* h_ai, const void* y,
+                      const double* noise_var, void* x_hat, float* llr, arches_stream_t stream);
+
+/* ---- Eq. 3 perturbation of the MMSE expert (perturbation_lab.py:92-98 +
+ * the Pipeline.perturb hook, phy_pipeline.py:401,444-445) --------------
+ * Run between arches_experts_equalize (K2 + K3) and arches_kpm_scan (K4) of a
+ * batch: for every stream with rho[stream] != 0 the MMSE output gets
+ * rho * mean|H_mmse| * CN(0,1) (CN from stream(seeds[stream], "inject", slot)
+ * in the reference's (A, 1, N, D) element order), is written back into h_mmse,
+ * re-equalised, and the MMSE candidate of tel (rsrp, SINR, MCS, TB, CRC, MAC
+ * bytes) is re-derived; abs_mean[1] stays the pre-injection mean (the hook's
+ * est_abs_mean).  rho == 0 streams are untouched.  tx complex64; slot
+ * numbering as arches_experts_equalize. */
+int arches_perturb_mmse(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                        int64_t first_slot, const double* rho, const uint64_t* seeds,
+                        const void* state, const void* y, const void* tx, const double* noise_var,
+                        void* h_mmse, arches_telemetry* tel, void* ws, arches_stream_t stream);
+
 /* ---- packed QPSK transmit grids (host <-> device wire format) -------
  * The genie transmit grid the equaliser scores against is QPSK everywhere
  * (qpsk(), rng.py:50-55, pilots included: radio_scene.py:240-249), so it

@@ -22,7 +22,7 @@ from paper_2604_23397_b200.config import (CB_SEGMENT_BITS, N_DATA_SYM, DappConfi
 from paper_2604_23397_b200.errors import (ConfigurationError, ContractViolation,
                                           EstimatorError, PipelineStateError)
 from paper_2604_23397_b200.geometry import GOOD, N_TAPS, pdp_powers
-from paper_2604_23397_b200.scene import lcid4_jitter, stream
+from paper_2604_23397_b200.scene import complex_normal, lcid4_jitter, stream
 
 RIDGE = 1e-12                          # expert_bank.py:19
 FEATURE_ORDER = ("phy_throughput", "mcs_index", "pdu_length", "ndi", "rsrp", "snr_db",
@@ -165,6 +165,56 @@ def equalize(y: np.ndarray, est: np.ndarray, noise_var: float, tx: np.ndarray, g
     err_p = np.vdot(err, err).real
     sinr = sinr_cap_db if err_p <= 0 else 10.0 * math.log10(abs(alpha) ** 2 * ref / err_p)
     return x_hat, min(sinr, sinr_cap_db)
+
+
+def equalizer_gain(est: np.ndarray, geo) -> np.ndarray:
+    """den - noise_var of equalize() (phy_pipeline.py:262-264): sum_a |h_interp|^2, (N, T)."""
+    a = time_interp_weights(tuple(geo.dmrs_symbols), geo.n_sym)
+    h = np.einsum("asd,td->ast", est[:, 0, :, :], a)
+    return np.einsum("ast,ast->st", np.conj(h), h).real
+
+
+# Gray PAM levels per dimension of TS 38.211 s5.1.3-5.1.5 (QPSK / 16QAM / 64QAM):
+# label bits (b_i, b_{i+2}, b_{i+4}) -> amplitude
+def _pam_levels(qm: int):
+    nb = qm // 2
+    scale = {2: 1 / math.sqrt(2.0), 4: 1 / math.sqrt(10.0), 6: 1 / math.sqrt(42.0)}[qm]
+    out = []
+    for lab in range(1 << nb):
+        c = [1 - 2 * ((lab >> i) & 1) for i in range(3)]
+        lev = c[0] if nb == 1 else c[0] * (2 - c[1]) if nb == 2 else c[0] * (4 - c[1] * (2 - c[2]))
+        out.append((lab, lev * scale))
+    return nb, out
+
+
+def demap_llr(x_hat: np.ndarray, gain: np.ndarray, noise_var: float, qm: int, geo) -> np.ndarray:
+    """Max-log LLRs log P(b=0)/P(b=1) of the data REs (the device K6 contract,
+    include/arches.h arches_downstream): z = x_hat / beta, beta = g / (g + nv),
+    noise variance nv / g; bit 2i from Re, 2i+1 from Im; (N, T, 6), zero on the
+    pilot REs (data_re_mask) and beyond qm."""
+    out = np.zeros(x_hat.shape + (6,))
+    if qm not in (2, 4, 6):
+        return out
+    nb, levels = _pam_levels(qm)
+    beta = gain / (gain + noise_var)
+    s2 = noise_var / gain
+    for comp, off in ((x_hat.real, 0), (x_hat.imag, 1)):
+        z = comp / beta
+        for i in range(nb):
+            d0 = np.min([(z - lev) ** 2 for lab, lev in levels if not (lab >> i) & 1], axis=0)
+            d1 = np.min([(z - lev) ** 2 for lab, lev in levels if (lab >> i) & 1], axis=0)
+            out[..., 2 * i + off] = (d1 - d0) / s2
+    out[~data_re_mask(geo)] = 0.0
+    return out
+
+
+def inject_values(values: np.ndarray, rho: float, seed: int, slot: int):
+    """perturbation_lab.py:92-98 -- Eq. 3: out = in + rho * mean|in| * CN(0,1)."""
+    m = float(np.mean(np.abs(values)))
+    if rho == 0.0:
+        return values.copy(), m
+    z = complex_normal(stream(seed, "inject", slot), values.shape)
+    return values + rho * m * z, m
 
 
 # ---------------------------------------------------------------- KPM layer
@@ -372,6 +422,7 @@ class SlotResult:
     downstream: np.ndarray | None = None
     mmse: np.ndarray | None = None
     ai: np.ndarray | None = None
+    x_hat: np.ndarray | None = None
 
 
 @dataclass
@@ -398,13 +449,16 @@ class CellLoop:
     def __init__(self, geo, scenarios, policy="oracle", exec_mode=ExecutionMode.CONCURRENT,
                  pcfg: PipelineConfig | None = None, dcfg: DappConfig | None = None,
                  latency: LatencyModel | None = None, tree_text: str | None = None,
-                 keep_arrays: bool = False):
+                 keep_arrays: bool = False, perturb_rho: float | None = None):
         self.geo, self.scenarios = geo, scenarios
         self.pcfg = pcfg or PipelineConfig()
         self.dcfg = dcfg or DappConfig()
         self.lat = latency or LatencyModel()
         self.exec_mode = exec_mode
         self.keep = keep_arrays
+        # Pipeline.perturb hook (phy_pipeline.py:401,444-445) as perturbation_lab.sweep
+        # installs it (perturbation_lab.py:127-133): Eq. 3 on the MMSE output
+        self.perturb_rho = perturb_rho
         self.slot_ns = geo.slot_duration_ns
         slot_s = geo.slot_duration_us * 1e-6
         self.ctl = SwitchController(exec_mode, self.slot_ns)
@@ -440,10 +494,13 @@ class CellLoop:
         else:
             to_run = (mode,)
         nv_est = mmse = ai = None
+        est_abs_mean = None
         for e in to_run:
             if e == 1:
                 nv_est = estimate_noise_var(ls, cfg.noise_guard)
                 mmse = mmse_estimate(ls, nv_est, scen.assumed_delay_spread, cfg.mmse_block_prbs)
+                if self.perturb_rho is not None:
+                    mmse, est_abs_mean = inject_values(mmse, self.perturb_rho, scen.seed, n)
                 self.buf[1] = mmse.copy()
             else:
                 ai = denoiser_estimate(ls, min(cfg.truncation, geo.n_sc))
@@ -455,9 +512,10 @@ class CellLoop:
         if mode == 1:
             self.buf[0] = self.buf[1].copy()
         down = self.buf[0]
-        est_abs_mean = float(np.mean(np.abs(down)))
+        if est_abs_mean is None:
+            est_abs_mean = float(np.mean(np.abs(down)))
         rsrp = float(np.mean(np.abs(down) ** 2))
-        _, sinr = equalize(y, down, nv, tx, geo, cfg.sinr_cap_db)
+        x_hat, sinr = equalize(y, down, nv, tx, geo, cfg.sinr_cap_db)
         tab = cfg.mcs_table
         mcs = link_adapt(sinr, tab)
         tb, rate, qam, ncb = transport_block(mcs, geo.n_prb, tab)
@@ -479,7 +537,8 @@ class CellLoop:
                         mac_t, l4_t, mac_rx, l4_rx)
         res = SlotResult(mode, sinr, est_abs_mean, rsrp, nv_est, crc, kpm,
                          down.copy() if self.keep else None,
-                         mmse if self.keep else None, ai if self.keep else None)
+                         mmse if self.keep else None, ai if self.keep else None,
+                         x_hat if self.keep else None)
         self.result.slots.append(res)
         self._control(regime, kpm)
         self.n += 1

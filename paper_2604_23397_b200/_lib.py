@@ -19,6 +19,7 @@ EXEC_CONCURRENT, EXEC_SELECTED_ONLY = 0, 1
 POLICY_ORACLE, POLICY_FIXED, POLICY_TREE = 0, 1, 2
 FLAG_NO_TC_K1, FLAG_NO_TC_K2 = 0x1, 0x2
 EXPERT_OUT_C128 = 0x100
+LLR_STRIDE = 6
 TRIGGERS = {0: "policy", 1: "failsafe", 2: "oracle", 3: "fixed"}
 
 
@@ -91,6 +92,9 @@ _SIGS = {
     "arches_ls_materialize": (C.c_int, [P, C.c_int32, P, P, P, P]),
     "arches_expert_from_ls": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, P, P, P]),
     "arches_equalize": (C.c_int, [P, C.c_int32, P, P, P, P, P, P, P, P, P, P]),
+    "arches_downstream": (C.c_int, [P, C.c_int32, P, P, P, P, P, P, P, P]),
+    "arches_perturb_mmse": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P,
+                                      P, P, P]),
     "arches_pack_qpsk": (C.c_int, [P, C.c_int32, P, P, P, P]),
     "arches_tx_bits_bytes": (C.c_size_t, [P, C.c_int32]),
     "arches_unpack_qpsk": (C.c_int, [P, C.c_int32, P, P, P]),

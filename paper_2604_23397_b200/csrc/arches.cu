@@ -20,6 +20,7 @@
 #include "k_control.cuh"
 #include "k_control_warp.cuh"
 #include "k_control_block.cuh"
+#include "k_downstream.cuh"
 #include "k_synth_eq.cuh"
 #include "k_synth_tc.cuh"
 #include "rng.cuh"
@@ -1046,6 +1047,61 @@ extern "C" int arches_switch_copy_one(const int32_t* mode, const void* src, void
   const unsigned blocks = (unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 1184));
   k5_switch_copy_one<<<blocks, 256, 0, s>>>(mode, reinterpret_cast<const float2*>(src),
                                             reinterpret_cast<float2*>(dst), n);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+// ------------------------------------------------------------ K6 / K7
+extern "C" int arches_downstream(const arches_plan* plan, int32_t n_units, const arches_kpm* kpm,
+                                 const void* h_mmse, const void* h_ai, const void* y,
+                                 const double* noise_var, void* x_hat, float* llr,
+                                 arches_stream_t stream) {
+  if (!plan || !kpm || !h_mmse || !h_ai || !y || !noise_var || n_units < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad downstream args");
+  if (!x_hat && !llr) return ARCHES_OK;
+  dim3 grid((plan->dev.N + K6_THREADS - 1) / K6_THREADS, n_units);
+  if (n_units > 65535) return set_err(ARCHES_E_CONTRACT, "downstream: at most 65535 units per call");
+  k6_xhat_demap<<<grid, K6_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      plan->dev, kpm, reinterpret_cast<const float2*>(h_mmse), reinterpret_cast<const float2*>(h_ai),
+      reinterpret_cast<const float2*>(y), noise_var, reinterpret_cast<float2*>(x_hat), llr, n_units);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_perturb_mmse(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                                   int64_t first_slot, const double* rho, const uint64_t* seeds,
+                                   const void* state, const void* y, const void* tx,
+                                   const double* noise_var, void* h_mmse, arches_telemetry* tel,
+                                   void* ws, arches_stream_t stream) {
+  if (!plan || !rho || !seeds || !y || !tx || !noise_var || !h_mmse || !tel || !ws ||
+      n_streams < 1 || n_slots < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad perturb_mmse args");
+  if (first_slot < 0 && !state)
+    return set_err(ARCHES_E_CONTRACT, "first_slot < 0 needs the stream state (slot source)");
+  const int n_units = n_streams * n_slots;
+  if (n_units > 65535) return set_err(ARCHES_E_CONTRACT, "perturb_mmse: at most 65535 units per call");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const WsLayout w = ws_layout(plan, n_units);
+  CUDA_TRY(cudaMemsetAsync(ws_at<void>(ws, w.counters), 0, n_units * sizeof(unsigned int), s));
+  static const uint64_t inject_key =
+      arches_rng::blake2b64(reinterpret_cast<const uint8_t*>("inject"), 6);
+  K7Args a;
+  a.rho = rho;
+  a.seeds = seeds;
+  a.inject_key = inject_key;
+  a.state = reinterpret_cast<const unsigned char*>(state);
+  a.state_stride = state_stride_bytes(plan->dev.window_length, plan->dev.dapp_window);
+  a.first_slot = first_slot;
+  a.n_slots = n_slots;
+  a.y = reinterpret_cast<const float2*>(y);
+  a.tx = reinterpret_cast<const float2*>(tx);
+  a.nv = noise_var;
+  a.h_mmse = reinterpret_cast<float2*>(h_mmse);
+  a.tel = tel;
+  a.parts = ws_at<TilePartial>(ws, w.parts);
+  a.counters = ws_at<unsigned int>(ws, w.counters);
+  dim3 grid((plan->dev.N + K6_THREADS - 1) / K6_THREADS, n_units);
+  k_perturb_mmse<<<grid, K6_THREADS, 0, s>>>(plan->dev, a);
   LAUNCH_CHECK();
   return ARCHES_OK;
 }

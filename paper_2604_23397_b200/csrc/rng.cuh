@@ -54,6 +54,31 @@ ARCHES_HD double stream_first_uniform(uint64_t seed, uint64_t purpose_key, uint6
   return (double)(c[0] >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// Generator.random() double number `idx` (0-based) of stream(seed, purpose, slot):
+// numpy's Philox buffers four outputs per counter, counter word 0 pre-incremented
+ARCHES_HD double stream_uniform_at(uint64_t seed, uint64_t purpose_key, uint64_t slot,
+                                   uint64_t idx) {
+  uint64_t c[4] = {1ull + (idx >> 2), slot, 0ull, 0ull};
+  philox4x64_10(c, seed, purpose_key);
+  return (double)(c[idx & 3] >> 11) * (1.0 / 9007199254740992.0);
+}
+
+#ifdef __CUDACC__
+// element e of complex_normal(stream(seed, purpose, slot), shape) with n elements
+// (rng.py:37-47): u1 = random #e, u2 = random #(n + e), sqrt(-log1p(-u1)) *
+// (cos, sin)(2 pi u2) -- numpy's operation order; libm-level (<= 2 ulp) rounding
+__device__ __forceinline__ double2 complex_normal_at(uint64_t seed, uint64_t purpose_key,
+                                                     uint64_t slot, uint64_t n, uint64_t e) {
+  const double u1 = stream_uniform_at(seed, purpose_key, slot, e);
+  const double u2 = stream_uniform_at(seed, purpose_key, slot, n + e);
+  const double r = sqrt(-log1p(-u1));
+  const double th = 6.283185307179586 * u2;  // (2j * np.pi) * u2: imaginary part
+  double sn, cs;
+  sincos(th, &sn, &cs);
+  return make_double2(r * cs, r * sn);
+}
+#endif
+
 ARCHES_HD uint64_t rotr64(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
 
 ARCHES_HD void b2_g(uint64_t* v, int a, int b, int c, int d, uint64_t x, uint64_t y) {

@@ -272,6 +272,55 @@ class SlotEngine:
             self._launch(-1)
         self.next_slot += self.S
 
+    def run_perturbed(self, rho):
+        """One batch with the Eq. 3 perturbation of the MMSE expert
+        (perturbation_lab.py:92-98 via the Pipeline.perturb hook, phy_pipeline.py:
+        444-445): K1 -> K2 + K3 -> K7 (inject rho[stream] * mean|H| * CN(0,1) into the
+        MMSE output, re-equalise, re-derive the MMSE candidate) -> K4.  rho: one
+        value per stream (rho = 0: untouched).  perturbation_lab.sweep is this
+        with one stream per rho point, MMSE selected (exec SELECTED_ONLY, no policy
+        traffic)."""
+        import torch
+        self._settle()
+        r = torch.as_tensor(np.broadcast_to(np.asarray(rho, dtype=np.float64), (self.C,)).copy(),
+                            device=self.device)
+        if bool((r < 0).any()) or bool((r > 2).any()):
+            raise ConfigurationError("rho values must lie in [0, 2]")
+        L, st, h = _lib.lib(), _stream_handle(), self.plan.handle
+        _lib.check(L.arches_ls_analyze(h, self.C, self.S, _lib.ptr(self.y), _lib.ptr(self.pilots),
+                                       None, -1, _lib.ptr(self.state), None, _lib.ptr(self.ws), st))
+        _lib.check(L.arches_experts_equalize(h, self.C, self.S, _lib.ptr(self.y), _lib.ptr(self.tx),
+                                             _lib.ptr(self.noise_var), _lib.ptr(self.seeds), -1,
+                                             _lib.ptr(self.state), _lib.ptr(self.h_mmse),
+                                             _lib.ptr(self.h_ai), _lib.ptr(self.tel),
+                                             _lib.ptr(self.ws), st))
+        _lib.check(L.arches_perturb_mmse(h, self.C, self.S, -1, _lib.ptr(r), _lib.ptr(self.seeds),
+                                         _lib.ptr(self.state), _lib.ptr(self.y), _lib.ptr(self.tx),
+                                         _lib.ptr(self.noise_var), _lib.ptr(self.h_mmse),
+                                         _lib.ptr(self.tel), _lib.ptr(self.ws), st))
+        _lib.check(L.arches_kpm_scan(h, self.C, self.S, _lib.ptr(self.tel), _lib.ptr(self.regime),
+                                     _lib.ptr(self.tree), _lib.ptr(self.state), _lib.ptr(self.kpm),
+                                     _lib.ptr(self.msg_log), _lib.ptr(self.msg_count), self.msg_cap,
+                                     st))
+        self.next_slot += self.S
+
+    def downstream_symbols(self, x_hat: bool = True, llr: bool = True):
+        """K6 after a run: x_hat (U, T, N) complex64 of each unit's SELECTED expert
+        (the switch predicate kpm.mode) as equalize() forms it, and max-log LLRs
+        (U, T, N, 6) for the slot's scheduled modulation (include/arches.h,
+        arches_downstream).  Returns device tensors (None where not requested)."""
+        import torch
+        self._settle()
+        xh = torch.empty((self.U, self.T, self.N), dtype=torch.complex64,
+                         device=self.device) if x_hat else None
+        lr = torch.empty((self.U, self.T, self.N, _lib.LLR_STRIDE), dtype=torch.float32,
+                         device=self.device) if llr else None
+        _lib.check(_lib.lib().arches_downstream(self.plan.handle, self.U, _lib.ptr(self.kpm),
+                                                _lib.ptr(self.h_mmse), _lib.ptr(self.h_ai),
+                                                _lib.ptr(self.y), _lib.ptr(self.noise_var),
+                                                _lib.ptr(xh), _lib.ptr(lr), _stream_handle()))
+        return xh, lr
+
     def join(self):
         """Order the current stream after any pending pipelined tail."""
         _lib.check(_lib.lib().arches_join(self.plan.handle, _stream_handle()))
