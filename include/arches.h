@@ -309,6 +309,28 @@ int arches_perturb_mmse(const arches_plan* plan, int32_t n_streams, int32_t n_sl
                         const void* state, const void* y, const void* tx, const double* noise_var,
                         void* h_mmse, arches_telemetry* tel, void* ws, arches_stream_t stream);
 
+/* ---- exhaustive depth-2 tree training (switch_policy.py:173-234) ------
+ * Scores root split candidates of a labelled dataset the way `train` does:
+ * for candidate c (feature root_feature[c], threshold root_threshold[c];
+ * feature -1 = no root split, the whole set is the "left" subset) the best
+ * depth-1 tree of each side (`_best_depth1`: every feature, every midpoint
+ * between consecutive distinct values of the SUBSET, first minimum per
+ * feature, strictly better feature wins) and its total leaf impurity
+ * (sum n * gini), fp64 in the reference's operation order.  The host picks
+ * the first minimum over candidates in (feature, threshold) order.
+ * xT[F][n] feature-major values; order[F][n] each column's stable ascending
+ * argsort; y[n] labels 0/1. */
+typedef struct arches_split_eval {
+  double total;            /* left_total + right_total */
+  double left_total, right_total;
+  double left_threshold, right_threshold;
+  int32_t left_feature, right_feature; /* -1: that side stays a leaf */
+} arches_split_eval;
+int arches_tree_eval_splits(const double* xT, const int32_t* order, const uint8_t* y, int32_t n,
+                            int32_t n_features, const int32_t* root_feature,
+                            const double* root_threshold, int32_t n_roots,
+                            arches_split_eval* out, arches_stream_t stream);
+
 /* ---- packed QPSK transmit grids (host <-> device wire format) -------
  * The genie transmit grid the equaliser scores against is QPSK everywhere
  * (qpsk(), rng.py:50-55, pilots included: radio_scene.py:240-249), so it

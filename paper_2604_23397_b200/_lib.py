@@ -64,6 +64,9 @@ KPM_DTYPE = np.dtype([
     ("est_abs_mean", "<f8"), ("mcs_index", "<i4"), ("pdu_length", "<i4"), ("ndi", "<i4"),
     ("qam_order", "<i4"), ("num_cb", "<i4"), ("tb_size", "<i4"), ("mac_rx_bytes", "<i4"),
     ("lcid4_rx_bytes", "<i4"), ("mode", "<i4"), ("crc_pass", "<i4")])
+SPLIT_EVAL_DTYPE = np.dtype([("total", "<f8"), ("left_total", "<f8"), ("right_total", "<f8"),
+                             ("left_threshold", "<f8"), ("right_threshold", "<f8"),
+                             ("left_feature", "<i4"), ("right_feature", "<i4")])
 MESSAGE_DTYPE = np.dtype([("decided_at_ns", "<i8"), ("deliverable_at_ns", "<i8"),
                           ("mode", "<i4"), ("trigger", "<i4")])
 assert TELEMETRY_DTYPE.itemsize == 104 and KPM_DTYPE.itemsize == 104
@@ -95,6 +98,7 @@ _SIGS = {
     "arches_downstream": (C.c_int, [P, C.c_int32, P, P, P, P, P, P, P, P]),
     "arches_perturb_mmse": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P,
                                       P, P, P]),
+    "arches_tree_eval_splits": (C.c_int, [P, P, P, C.c_int32, C.c_int32, P, P, C.c_int32, P, P]),
     "arches_pack_qpsk": (C.c_int, [P, C.c_int32, P, P, P, P]),
     "arches_tx_bits_bytes": (C.c_size_t, [P, C.c_int32]),
     "arches_unpack_qpsk": (C.c_int, [P, C.c_int32, P, P, P]),

@@ -21,6 +21,7 @@
 #include "k_control_warp.cuh"
 #include "k_control_block.cuh"
 #include "k_downstream.cuh"
+#include "k_tree_train.cuh"
 #include "k_synth_eq.cuh"
 #include "k_synth_tc.cuh"
 #include "rng.cuh"
@@ -1102,6 +1103,21 @@ extern "C" int arches_perturb_mmse(const arches_plan* plan, int32_t n_streams, i
   a.counters = ws_at<unsigned int>(ws, w.counters);
   dim3 grid((plan->dev.N + K6_THREADS - 1) / K6_THREADS, n_units);
   k_perturb_mmse<<<grid, K6_THREADS, 0, s>>>(plan->dev, a);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+// ------------------------------------------------------------ tree training
+extern "C" int arches_tree_eval_splits(const double* xT, const int32_t* order, const uint8_t* y,
+                                       int32_t n, int32_t n_features, const int32_t* root_feature,
+                                       const double* root_threshold, int32_t n_roots,
+                                       arches_split_eval* out, arches_stream_t stream) {
+  if (!xT || !order || !y || !root_feature || !root_threshold || !out || n < 1 ||
+      n_features < 1 || n_roots < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad tree_eval_splits args");
+  const unsigned blocks = (unsigned)((n_roots + TT_WARPS - 1) / TT_WARPS);
+  k_tree_eval_splits<<<blocks, 32 * TT_WARPS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      xT, order, y, n, n_features, root_feature, root_threshold, n_roots, out);
   LAUNCH_CHECK();
   return ARCHES_OK;
 }
