@@ -331,6 +331,37 @@ int arches_tree_eval_splits(const double* xT, const int32_t* order, const uint8_
                             const double* root_threshold, int32_t n_roots,
                             arches_split_eval* out, arches_stream_t stream);
 
+/* ---- device-side slot synthesis (input generation) -----
+ * The reference scene (rng.py:24-55, radio_scene.py:140-306, driven as
+ * Pipeline.run_slot does, phy_pipeline.py:430-433,459) for n_streams cells x
+ * n_slots consecutive slots: AR(1) TDL channel + log-normal shadow, delayed
+ * interferer, pilots, QPSK data, Y = H X + sqrt(nv) W + sqrt(iv) H_i X_i -- every
+ * Philox stream keyed and indexed as numpy does (bits exact; fp64 libm / DFT
+ * rounding within ulps).  Per-stream AR(1) state lives in scene_state (zeroed =
+ * slot 0).  regimes[2]: 0 = poor, 1 = good (the engine's regime codes); the
+ * unit's regime[u] picks one.  shadow_z[u] = stream(seed, "shadow", slot).
+ * standard_normal() (numpy's ziggurat; host-drawn, one per cell-slot).
+ * Outputs y[u][A][T][N], tx[u][T][N] complex64, noise_var[u]. */
+typedef struct arches_scene_regime {
+  double noise_var;             /* ScenarioConfig.noise_var(n_ant) */
+  double interference_var;      /* ScenarioConfig.interference_var() */
+  double temporal_correlation;
+  double shadow_sigma_db;
+  double shadow_correlation;
+} arches_scene_regime;
+size_t arches_scene_state_bytes(const arches_plan* plan, int32_t n_streams);
+size_t arches_scene_workspace_bytes(const arches_plan* plan, int32_t n_units);
+/* pilot_sequence (radio_scene.py:233-237) of every stream: pilots[stream][M][D] */
+int arches_scene_pilots(const arches_plan* plan, int32_t n_streams, const uint64_t* seeds,
+                        void* pilots, arches_stream_t stream);
+int arches_synthesize(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                      const uint64_t* seeds, const arches_scene_regime* regimes /* host [2] */,
+                      const uint8_t* prb_mask /* device [2][n_prb] */,
+                      const double* sqrt_pdp /* host [8] */, int32_t excess_delay,
+                      const int8_t* regime, const double* shadow_z, const void* pilots,
+                      void* scene_state, void* scene_ws, void* y, void* tx, double* noise_var,
+                      arches_stream_t stream);
+
 /* ---- packed QPSK transmit grids (host <-> device wire format) -------
  * The genie transmit grid the equaliser scores against is QPSK everywhere
  * (qpsk(), rng.py:50-55, pilots included: radio_scene.py:240-249), so it

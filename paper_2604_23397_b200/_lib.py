@@ -44,6 +44,12 @@ class Params(C.Structure):
                 ("failsafe_timeout_ns", C.c_int64), ("crc_purpose_key", C.c_uint64)]
 
 
+class SceneRegime(C.Structure):
+    _fields_ = [("noise_var", C.c_double), ("interference_var", C.c_double),
+                ("temporal_correlation", C.c_double), ("shadow_sigma_db", C.c_double),
+                ("shadow_correlation", C.c_double)]
+
+
 class TreeNode(C.Structure):
     _fields_ = [("feature", C.c_int32), ("left", C.c_int32), ("right", C.c_int32),
                 ("label", C.c_int32), ("threshold", C.c_double)]
@@ -99,6 +105,11 @@ _SIGS = {
     "arches_perturb_mmse": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, P, P, P, P, P, P, P,
                                       P, P, P]),
     "arches_tree_eval_splits": (C.c_int, [P, P, P, C.c_int32, C.c_int32, P, P, C.c_int32, P, P]),
+    "arches_scene_state_bytes": (C.c_size_t, [P, C.c_int32]),
+    "arches_scene_workspace_bytes": (C.c_size_t, [P, C.c_int32]),
+    "arches_scene_pilots": (C.c_int, [P, C.c_int32, P, P, P]),
+    "arches_synthesize": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, P, C.c_int32, P, P, P, P,
+                                    P, P, P, P, P]),
     "arches_pack_qpsk": (C.c_int, [P, C.c_int32, P, P, P, P]),
     "arches_tx_bits_bytes": (C.c_size_t, [P, C.c_int32]),
     "arches_unpack_qpsk": (C.c_int, [P, C.c_int32, P, P, P]),

@@ -328,12 +328,38 @@ def predict(tree, x):
         raise _E.ContractViolation(str(e)) from None
 
 
+def train(data, max_depth: int = 2):
+    """switch_policy.train (switch_policy.py:173-234) with the exhaustive root
+    search on the device (paper_2604_23397_b200.train); same tree, same errors,
+    the caller's Node / TreeModel classes."""
+    from . import train as _train
+    from .policy import Node as _Node
+    if len(data) == 0:
+        raise _E.ContractViolation("cannot train on an empty dataset")
+    try:
+        tree = _train.train(data.x, data.y, max_depth=max_depth,
+                            feature_names=tuple(data.feature_names))
+    except _own_errors.ConfigurationError as e:
+        raise _E.ConfigurationError(str(e)) from None
+    except _own_errors.ContractViolation as e:
+        raise _E.ContractViolation(str(e)) from None
+    node_cls, model_cls = _CLASSES.get("Node", _Node), _CLASSES.get("TreeModel", type(tree))
+
+    def conv(n):
+        if n is None:
+            return None
+        return node_cls(counts=tuple(n.counts), feature=n.feature, threshold=n.threshold,
+                        left=conv(n.left), right=conv(n.right))
+    return model_cls(conv(tree.root), tuple(data.feature_names))
+
+
 # ---------------------------------------------------------------- install
 
 NAMES_PHY = ("ls_estimate", "estimate_noise_var", "mmse_estimate", "denoiser_estimate",
              "switch_select", "equalize", "ExpertBuffers")
 NAMES_EXPERT_BANK = ("ls_estimate", "estimate_noise_var", "mmse_estimate", "denoiser_estimate")
 NAMES_DAPP = ("window_features", "predict")
+NAMES_POLICY = ("train",)
 
 
 def install(package=None) -> dict:
@@ -346,7 +372,7 @@ def install(package=None) -> dict:
     me = sys.modules[__name__]
     saved = {}
     for modname, names in (("phy_pipeline", NAMES_PHY), ("expert_bank", NAMES_EXPERT_BANK),
-                           ("dapp_control", NAMES_DAPP)):
+                           ("dapp_control", NAMES_DAPP), ("switch_policy", NAMES_POLICY)):
         mod = getattr(pkg, modname, None)
         if mod is None:
             continue
@@ -362,6 +388,9 @@ def install(package=None) -> dict:
     eb = getattr(pkg, "expert_bank", None)
     if eb is not None:
         _CLASSES.update(DmrsEstimate=eb.DmrsEstimate, Stage=eb.Stage, ExpertId=eb.ExpertId)
+    sp = getattr(pkg, "switch_policy", None)
+    if sp is not None:
+        _CLASSES.update(Node=sp.Node, TreeModel=sp.TreeModel)
     return saved
 
 
@@ -371,3 +400,5 @@ def uninstall(package, saved: dict):
         setattr(getattr(package, modname), n, fn)
     _E = _own_errors
     _CLASSES.update(DmrsEstimate=_OwnDmrsEstimate, Stage=_OwnStage, ExpertId=_OwnExpertId)
+    _CLASSES.pop("Node", None)
+    _CLASSES.pop("TreeModel", None)

@@ -22,6 +22,7 @@
 #include "k_control_block.cuh"
 #include "k_downstream.cuh"
 #include "k_tree_train.cuh"
+#include "k_scene.cuh"
 #include "k_synth_eq.cuh"
 #include "k_synth_tc.cuh"
 #include "rng.cuh"
@@ -1103,6 +1104,82 @@ extern "C" int arches_perturb_mmse(const arches_plan* plan, int32_t n_streams, i
   a.counters = ws_at<unsigned int>(ws, w.counters);
   dim3 grid((plan->dev.N + K6_THREADS - 1) / K6_THREADS, n_units);
   k_perturb_mmse<<<grid, K6_THREADS, 0, s>>>(plan->dev, a);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+// ------------------------------------------------------------ scene synthesis
+static uint64_t purpose_key64(const char* p) {
+  return arches_rng::blake2b64(reinterpret_cast<const uint8_t*>(p), (int)strlen(p));
+}
+
+extern "C" size_t arches_scene_state_bytes(const arches_plan* plan, int32_t n_streams) {
+  return plan && n_streams > 0 ? (size_t)n_streams * scene_state_stride(plan->dev.A) : 0;
+}
+
+extern "C" size_t arches_scene_workspace_bytes(const arches_plan* plan, int32_t n_units) {
+  return plan && n_units > 0 ? (size_t)n_units * 2 * plan->dev.A * SCENE_TAPS * sizeof(double2) : 0;
+}
+
+extern "C" int arches_scene_pilots(const arches_plan* plan, int32_t n_streams, const uint64_t* seeds,
+                                   void* pilots, arches_stream_t stream) {
+  if (!plan || !seeds || !pilots || n_streams < 1) return set_err(ARCHES_E_CONTRACT, "bad scene_pilots args");
+  const int MD = plan->dev.M * plan->dev.D;
+  dim3 grid((MD + 127) / 128, n_streams);
+  k_scene_pilots<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      plan->dev, seeds, purpose_key64("pilot"), reinterpret_cast<float2*>(pilots), n_streams);
+  LAUNCH_CHECK();
+  return ARCHES_OK;
+}
+
+extern "C" int arches_synthesize(const arches_plan* plan, int32_t n_streams, int32_t n_slots,
+                                 const uint64_t* seeds, const arches_scene_regime* regimes,
+                                 const uint8_t* prb_mask, const double* sqrt_pdp,
+                                 int32_t excess_delay, const int8_t* regime, const double* shadow_z,
+                                 const void* pilots, void* scene_state, void* scene_ws, void* y,
+                                 void* tx, double* noise_var, arches_stream_t stream) {
+  if (!plan || !seeds || !regimes || !prb_mask || !sqrt_pdp || !regime || !shadow_z || !pilots ||
+      !scene_state || !scene_ws || !y || !tx || !noise_var || n_streams < 1 || n_slots < 1)
+    return set_err(ARCHES_E_CONTRACT, "bad synthesize args");
+  const PlanDev& d = plan->dev;
+  if (d.A * SCENE_TAPS > 1024) return set_err(ARCHES_E_CONFIG, "synthesize: n_ant > 128");
+  const int n_units = n_streams * n_slots;
+  if (n_units > 65535) return set_err(ARCHES_E_CONTRACT, "synthesize: at most 65535 units per call");
+  if (excess_delay < 0 || excess_delay + SCENE_TAPS > d.M)
+    return set_err(ARCHES_E_CONFIG, "interference_excess_delay does not fit the comb span");
+  SceneArgs a;
+  memset(&a, 0, sizeof(a));
+  a.seeds = seeds;
+  for (int r = 0; r < 2; ++r) {
+    a.reg[r].noise_var = regimes[r].noise_var;
+    a.reg[r].interference_var = regimes[r].interference_var;
+    a.reg[r].temporal_correlation = regimes[r].temporal_correlation;
+    a.reg[r].shadow_sigma_db = regimes[r].shadow_sigma_db;
+    a.reg[r].shadow_correlation = regimes[r].shadow_correlation;
+  }
+  a.prb_mask = prb_mask;
+  for (int l = 0; l < SCENE_TAPS; ++l) a.sqrt_p[l] = sqrt_pdp[l];
+  a.excess_delay = excess_delay;
+  a.shadowed = 1;
+  a.regime = regime;
+  a.shadow_z = shadow_z;
+  a.state = reinterpret_cast<unsigned char*>(scene_state);
+  a.taps_u = reinterpret_cast<double2*>(scene_ws);
+  a.y = reinterpret_cast<float2*>(y);
+  a.tx = reinterpret_cast<float2*>(tx);
+  a.noise_var = noise_var;
+  a.n_slots = n_slots;
+  a.key_channel = purpose_key64("channel");
+  a.key_interferer = purpose_key64("interferer");
+  a.key_awgn = purpose_key64("awgn");
+  a.key_data = purpose_key64("data");
+  a.key_idata = purpose_key64("interferer-data");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int th = ((d.A * SCENE_TAPS + 31) / 32) * 32;
+  k_scene_taps<<<n_streams, th, 0, s>>>(d, a);
+  LAUNCH_CHECK();
+  dim3 grid((d.N + 127) / 128, n_units);
+  k_scene_grid<<<grid, 128, 0, s>>>(d, a, reinterpret_cast<const float2*>(pilots), n_units);
   LAUNCH_CHECK();
   return ARCHES_OK;
 }
