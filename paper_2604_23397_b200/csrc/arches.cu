@@ -1227,6 +1227,7 @@ extern "C" int arches_unpack_qpsk(const arches_plan* plan, int32_t n_units, cons
   if (!plan || !tx || !tx_bits || n_units < 1)
     return set_err(ARCHES_E_CONTRACT, "bad unpack_qpsk args");
   const size_t n_bytes = arches_tx_bits_bytes(plan, n_units);
+  if (n_bytes >= (1ull << 32)) return set_err(ARCHES_E_CONTRACT, "unpack_qpsk: batch too large");
   k_unpack_qpsk<<<qpsk_blocks(plan, n_bytes), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       plan->dev, reinterpret_cast<const unsigned char*>(tx_bits), reinterpret_cast<float2*>(tx),
       n_bytes);

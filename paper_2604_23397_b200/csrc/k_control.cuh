@@ -290,14 +290,15 @@ __global__ void k_pack_qpsk(const PlanDev P, const float2* tx, unsigned char* bi
 // packed QPSK codes -> the complex64 grid tx[u][T][N]; one thread per code byte
 __global__ void k_unpack_qpsk(const PlanDev P, const unsigned char* bits, float2* tx, size_t n_bytes) {
   const float q = __uint_as_float(ARCHES_QPSK_AMP);
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bytes;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const size_t row = i / ARCHES_TXB_ROW;  // (u, tile, t)
+  // 32-bit index arithmetic (callers stay below 2^32 code bytes: 1.4e6 units at 273 PRB)
+  for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < (unsigned int)n_bytes;
+       i += gridDim.x * blockDim.x) {
+    const unsigned int row = i / ARCHES_TXB_ROW;  // (u, tile, t)
     const int jb = (int)(i - row * ARCHES_TXB_ROW);
-    const int t = (int)(row % P.T);
-    const size_t ut = row / P.T;
-    const int tile = (int)(ut % P.n_tiles);
-    const size_t u = ut / P.n_tiles;
+    const int t = (int)(row % (unsigned)P.T);
+    const unsigned int ut = row / (unsigned)P.T;
+    const int tile = (int)(ut % (unsigned)P.n_tiles);
+    const size_t u = ut / (unsigned)P.n_tiles;
     const unsigned int code = bits[i];
     float2* dst = tx + (u * P.T + t) * (size_t)P.N;
     for (int r = 0; r < 4; ++r) {

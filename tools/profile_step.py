@@ -18,15 +18,17 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--n-prb", type=int, default=273)
     ap.add_argument("--n-ant", type=int, default=4)
+    ap.add_argument("--streams", type=int, default=1)
     a = ap.parse_args()
     import torch
-    from bench import make_inputs
+    from bench import make_stream_inputs
     from paper_2604_23397_b200.config import ExecutionMode, PipelineConfig
     from paper_2604_23397_b200.engine import ArchesPlan, SlotEngine
-    geo, scens, pil, y, tx, nv, reg = make_inputs(a.n_prb, a.n_ant, a.slots, 1000)
+    seeds = [1000 + k for k in range(a.streams)]
+    geo, scens, pil, y, tx, nv, reg = make_stream_inputs(a.n_prb, a.n_ant, a.slots, seeds)
     plan = ArchesPlan(geo, 1.25, PipelineConfig(), ExecutionMode.CONCURRENT, "oracle")
-    eng = SlotEngine(plan, 1, a.slots)
-    eng.set_streams(pil[None], [1000])
+    eng = SlotEngine(plan, a.streams, a.slots)
+    eng.set_streams(pil, seeds)
     eng.load(y=y, tx=tx, noise_var=nv, regime=reg)
     for _ in range(a.steps):
         eng.run()
