@@ -394,11 +394,14 @@ __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev 
     acc[o2] = sum;
     if (cc < 2 * P.guard) sg += sum * sum;
   }
+  // row energies: thread = (a, d, part), every load in flight at once (a per-thread
+  // loop over the parts serialises one L2 round trip per part)
   double e = 0.0;
-  for (int o2 = tid; o2 < AD; o2 += K1T_FIN_THREADS) {
-    const int aa = o2 / P.D, d = o2 - aa * P.D;
+  for (int o2 = tid; o2 < AD * np; o2 += K1T_FIN_THREADS) {
+    const int ad = o2 / np, q = o2 - ad * np;
+    const int aa = ad / P.D, d = ad - aa * P.D;
     const int row = u * P.A + aa, g = row / 128, r = row - g * 128;
-    for (int q = 0; q < np; ++q) e += __ldcg(a.epart + (size_t)((q * P.D + d) * a.n_g + g) * 128 + r);
+    e += __ldcg(a.epart + (size_t)((q * P.D + d) * a.n_g + g) * 128 + r);
   }
   e = warp_sum(e);
   sg = warp_sum(sg);
