@@ -130,13 +130,20 @@ def relaunch(argv, n):
 
 
 # ------------------------------------------------------------------ CPU (oracle)
+def _ref_module():
+    """The reference's own code when staged (baseline/_ref, tools/fetch_ref.py): kind
+    "reference"; otherwise the pinned oracle port (oracle/cpu_bench.py): kind "port"."""
+    from oracle.ref_bench import staged
+    return ("oracle.ref_bench", "reference") if staged() else ("oracle.cpu_bench", "port")
+
+
 def _cpu_run(procs: int, slots: int, threads: int, extra):
-    """Run `procs` oracle processes concurrently; returns list of per-proc JSON."""
+    """Run `procs` CPU-baseline processes concurrently; returns list of per-proc JSON."""
     env = dict(os.environ)
     for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
         env[k] = str(threads)
     env["CUDA_VISIBLE_DEVICES"] = ""
-    ps = [subprocess.Popen([sys.executable, "-m", "oracle.cpu_bench", "--slots", str(slots),
+    ps = [subprocess.Popen([sys.executable, "-m", _ref_module()[0], "--slots", str(slots),
                             "--seed", str(i), *extra], cwd=ROOT, env=env,
                            stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
           for i in range(procs)]
@@ -144,7 +151,7 @@ def _cpu_run(procs: int, slots: int, threads: int, extra):
     for p in ps:
         o, e = p.communicate()
         if p.returncode != 0:
-            raise RuntimeError(f"oracle cpu_bench failed: {e[-2000:]}")
+            raise RuntimeError(f"{_ref_module()[0]} failed: {e[-2000:]}")
         out.append(json.loads(o.strip().splitlines()[-1]))
     return out
 
@@ -156,16 +163,19 @@ def cpu_reference_rate(a, warm, timed):
     cores = os.cpu_count() or 1
     procs = min(cores, 64)
     extra = ["--n-prb", str(a.n_prb), "--n-ant", str(a.n_ant), "--policy", a.policy]
+    what = ("the reference's own Pipeline.run_slot loop (staged ranswitch)"
+            if _ref_module()[1] == "reference" else "the pinned oracle port")
     if a.policy == "tree":
         extra += ["--tree", a.tree]
     res = {}
     r = _cpu_run(procs, warm + timed, 1, extra)
     t = max(sum(x["per_slot_s"][warm:]) for x in r)
-    res["multiproc"] = (procs * timed / t, procs, f"{procs} procs x 1 BLAS thread x {timed} timed "
-                        f"slots each (+{warm} warm-up); a step = one slot per process", t / timed)
+    res["multiproc"] = (procs * timed / t, procs, f"{what}: {procs} procs x 1 BLAS thread x {timed} "
+                        f"timed slots each (+{warm} warm-up); a step = one slot per process",
+                        t / timed)
     r = _cpu_run(1, warm + timed, cores, extra)
     t = sum(r[0]["per_slot_s"][warm:])
-    res["blas"] = (timed / t, cores, f"1 proc x {cores} BLAS threads x {timed} timed slots "
+    res["blas"] = (timed / t, cores, f"{what}: 1 proc x {cores} BLAS threads x {timed} timed slots "
                    f"(+{warm} warm-up); a step = one slot", t / timed)
     best = max(res.values(), key=lambda v: v[0])
     return best, res
@@ -180,7 +190,7 @@ def cpu_policy_rate(a, warm, timed):
                                           "--tree", a.tree])
     t = max(sum(x["per_boundary_s"][warm:]) for x in r)
     rate = cores * sample * timed / t           # cell-decisions per second
-    return rate, cores, (f"{cores} procs x {sample} cells x {timed} boundaries "
+    return rate, cores, (f"{_ref_module()[0]}: {cores} procs x {sample} cells x {timed} boundaries "
                          f"(+{warm} warm-up); a step = one boundary of {sample} cells per process"), \
         t / timed
 
@@ -205,7 +215,7 @@ def run_reference_arm(a, rank, world):
             "ms_per_step": 1000.0 * s_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128/f64", "data": "synthetic", "impl": "reference",
             "config": workload(a, world),
-            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": _ref_module()[1],
                              "sample": sample, "alternatives": alts},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -525,8 +535,8 @@ def run_ours(a, rank, world, backend):
         cpu = None
         if world == 1 and not a.no_cpu_baseline:
             (rate, cores, sample, _), allres = cpu_reference_rate(a, 1, 2)
-            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
-                   "alternatives": {k: v[0] for k, v in allres.items()}}
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": _ref_module()[1],
+                   "sample": sample, "alternatives": {k: v[0] for k, v in allres.items()}}
         line = {
             "metric": metric_name(a), "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": t_max / K, "higher_is_better": True, "scaling": "weak",
@@ -663,7 +673,7 @@ def run_policy_stress(a, rank, world, backend):
         cpu = None
         if world == 1 and not a.no_cpu_baseline:
             rate, cores, sample, _ = cpu_policy_rate(a, 1, 3)
-            cpu = {"value": rate, "unit": "decisions/s", "cores": cores, "kind": "port",
+            cpu = {"value": rate, "unit": "decisions/s", "cores": cores, "kind": _ref_module()[1],
                    "sample": sample}
         us_b = t_max / K * 1000.0
         line = {"metric": metric_name(a), "value": units / (t_max / 1000.0), "unit": "decisions/s",
