@@ -152,7 +152,9 @@ __device__ __forceinline__ void eq_re(const float2 (&h)[NA][ND], const float* wt
     float2 hn = make_float2(0.f, 0.f);
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
-      if (wt[d] != 0.f) {  // folds away for compile-time weights
+      if (wt[d] == 1.f) {  // a held symbol: the DMRS estimate itself (compile-time weights)
+        hn = h[a][d];
+      } else if (wt[d] != 0.f) {  // folds away for compile-time weights
         hn.x = fmaf(wt[d], h[a][d].x, hn.x);
         hn.y = fmaf(wt[d], h[a][d].y, hn.y);
       }
@@ -255,7 +257,9 @@ __device__ __forceinline__ void eq_grp_half(const float2 (&h)[NA][ND], const flo
       float2 hn = make_float2(0.f, 0.f);
 #pragma unroll
       for (int d = 0; d < ND; ++d) {
-        if (wt[d] != 0.f) {
+        if (wt[d] == 1.f) {
+          hn = h[a][d];
+        } else if (wt[d] != 0.f) {
           hn.x = fmaf(wt[d], h[a][d].x, hn.x);
           hn.y = fmaf(wt[d], h[a][d].y, hn.y);
         }
