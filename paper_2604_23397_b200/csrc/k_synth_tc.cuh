@@ -194,14 +194,63 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, u
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
 }
 
+// one RE of the NR 0/5/10 pattern with the MRC denominator given:
+// den = sum_a |w0 h_d0 + w1 h_d1|^2 from the DMRS Gram entries (eq_std_half)
+template <int NA, int ND>
+__device__ __forceinline__ void eq_re_den(const float2 (&h)[NA][ND], const float* wt,
+                                          const float2* yv, float2 x, float m, float den_nv,
+                                          float& sre, float& sim, float& syy) {
+  float2 num = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int a = 0; a < NA; ++a) {
+    float2 hn = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      if (wt[d] == 1.f) {
+        hn = h[a][d];
+      } else if (wt[d] != 0.f) {
+        hn.x = fmaf(wt[d], h[a][d].x, hn.x);
+        hn.y = fmaf(wt[d], h[a][d].y, hn.y);
+      }
+    }
+    num.x = fmaf(hn.x, yv[a].x, fmaf(hn.y, yv[a].y, num.x));
+    num.y = fmaf(hn.x, yv[a].y, fmaf(-hn.y, yv[a].x, num.y));
+  }
+  float inv;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(den_nv));
+  inv *= m;  // m = 0 on pilot REs
+  const float hr = num.x * inv, hi = num.y * inv;
+  sre = fmaf(x.x, hr, fmaf(x.y, hi, sre));
+  sim = fmaf(x.x, hi, fmaf(-x.y, hr, sim));
+  syy = fmaf(hr, hr, fmaf(hi, hi, syy));
+}
+
 // one symbol half (H) of the NR 0/5/10 pattern for one expert thread; SXX:
-// this thread also accumulates |x|^2 (expert-0 threads)
+// this thread also accumulates |x|^2 (expert-0 threads).  The MRC denominators
+// come from the DMRS Gram entries G_dd = sum_a |h_ad|^2 and R = sum_a Re(h_ad^*
+// h_a,d+1) of the half's DMRS pair: a held symbol's is G_dd (the same fma chain
+// as the direct sum), an interpolated one's w0^2 G00 + w1^2 G11 + 2 w0 w1 R.
 template <int NA, int ND, int H, bool SXX>
 __device__ __forceinline__ void eq_std_half(const float2 (&h)[NA][ND], const float2* yrow,
                                             const float2* xrow, float modd, float nv, float& sre,
                                             float& sim, float& syy, float& sxx) {
   // balanced halves: 4 interpolated + 3 held symbols each
   constexpr int kSym[2][7] = {{0, 1, 2, 3, 4, 5, 10}, {6, 7, 8, 9, 11, 12, 13}};
+  static_assert(ND == 3, "NR 0/5/10 pattern");
+  float g[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    g[d] = 0.f;
+    if (H == 0 || d > 0) {
+#pragma unroll
+      for (int a = 0; a < NA; ++a) g[d] = fmaf(h[a][d].x, h[a][d].x, fmaf(h[a][d].y, h[a][d].y, g[d]));
+    }
+  }
+  constexpr int d0 = H == 0 ? 0 : 1;  // the half's interpolated DMRS pair (d0, d0 + 1)
+  float r = 0.f;
+#pragma unroll
+  for (int a = 0; a < NA; ++a)
+    r = fmaf(h[a][d0].x, h[a][d0 + 1].x, fmaf(h[a][d0].y, h[a][d0 + 1].y, r));
 #pragma unroll
   for (int tt = 0; tt < 7; ++tt) {
     const int t = kSym[H][tt];
@@ -214,7 +263,15 @@ __device__ __forceinline__ void eq_std_half(const float2 (&h)[NA][ND], const flo
     const float2 x = xrow[(size_t)t * ARCHES_TILE];
     const bool dm = (t == 0 || t == 5 || t == 10);
     const float m = dm ? modd : 1.f;
-    eq_re<NA, ND>(h, wt, yv, x, m, nv, sre, sim, syy);
+    float den;
+    if (wt[0] == 1.f) den = g[0];
+    else if (wt[1] == 1.f) den = g[1];
+    else if (wt[2] == 1.f) den = g[2];
+    else {
+      const float w0 = wt[d0], w1 = wt[d0 + 1];
+      den = fmaf(w0 * w0, g[d0], fmaf(w1 * w1, g[d0 + 1], (2.f * w0 * w1) * r));
+    }
+    eq_re_den<NA, ND>(h, wt, yv, x, m, den + nv, sre, sim, syy);
     if (SXX) {
       if (dm) sxx = fmaf(m * x.x, x.x, fmaf(m * x.y, x.y, sxx));
       else sxx = fmaf(x.x, x.x, fmaf(x.y, x.y, sxx));
@@ -595,7 +652,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       const float modd = (kk & 1) ? 1.f : 0.f;  // pilot REs: even k on DMRS symbols
       const float2* yrow = sYX + (size_t)buf * stage_elems + j;
       const float2* xrow = yrow + (size_t)AS * T * ARCHES_TILE;
-      if (kGrp) {  // antenna groups: MRC sums across the tile's groups, finalised at the last
+      if constexpr (kGrp) {  // antenna groups: MRC sums across the tile's groups, finalised at the last
         const bool first = gr == 0, last = gr + 1 == ngrp;
         if (half == 0) {
           if (ex == 0) eq_grp_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
@@ -604,7 +661,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
           if (ex == 0) eq_grp_half<NA, ND, 1, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
           else         eq_grp_half<NA, ND, 1, false>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
         }
-      } else if (kStd) {  // compile-time symbol half and expert: weights and pilot symbols fold
+      } else if constexpr (kStd) {  // compile-time symbol half and expert: weights and pilot symbols fold
         if (half == 0) {
           if (ex == 0) eq_std_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
           else         eq_std_half<NA, ND, 0, false>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
