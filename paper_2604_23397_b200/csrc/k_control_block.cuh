@@ -16,6 +16,8 @@
 //   3. at a decision slot threads 0..9 form the window means (sequential fp64
 //      column sums in slot order), thread 0 runs the tree.
 #pragma once
+#include <limits.h>
+
 #include "k_control_warp.cuh"
 
 #define K4B_THREADS 256
@@ -125,6 +127,80 @@ __global__ void __launch_bounds__(K4B_THREADS) k4_kpm_scan_block(const PlanDev P
       }
       __syncthreads();
       if (tid == 0 && a.msg_count) a.msg_count[stream] = cnt0 + (int)s_tmp[0];
+    } else if (P.policy != ARCHES_POLICY_ORACLE && lim > 8) {
+      // tree / fixed sources, slot-parallel: between two dApp decisions the queues
+      // only drain (plus at most one fail-safe trip), so every slot's mode is the
+      // latest queued event applied by then -- key (apply slot, pending < forced,
+      // queue order) -- and the trip is the first slot whose predicate holds
+      // (SwitchController.begin_slot, phy_pipeline.py:123-139; FailsafeMonitor,
+      // dapp_control.py:123-149).  Same states and logs as the sequential walk,
+      // which still serves short chunks (a decision every slot: fewer barriers).
+      const StreamState& st = s_st;
+      const int64_t nbase = st.next_slot;
+      const bool sel = P.exec_mode == ARCHES_EXEC_SELECTED_ONLY;
+      int len = lim, decide = 0;
+      if (P.policy == ARCHES_POLICY_TREE) {
+        const int jd = max(0, P.decision_period - st.since_decision - 1);  // the decision slot
+        if (jd < lim) {
+          len = jd + 1;
+          decide = 1;
+        }
+      }
+      const int np = st.n_pending, nf = st.n_forced;
+      const int64_t n = nbase + tid;
+      // apply slot of a message: first slot whose begin time passes it
+      auto ceil_slot = [&](int64_t at) { return at <= 0 ? (int64_t)0 : (at + slot_ns - 1) / slot_ns; };
+      int best_s = -1, best_k = -1, best_i = -1, mode = st.mode;
+      auto consider = [&](int64_t as, int kind, int i, int m) {
+        if (as > n) return;
+        const int asi = (int)(as - nbase);
+        if (asi > best_s || (asi == best_s && (kind > best_k || (kind == best_k && i > best_i)))) {
+          best_s = asi;
+          best_k = kind;
+          best_i = i;
+          mode = m;
+        }
+      };
+      if (tid < len) {
+        for (int i = 0; i < np; ++i)
+          consider(ceil_slot(st.pending[i].at_ns) + (sel ? 1 : 0), 0, i, st.pending[i].mode);
+        for (int i = 0; i < nf; ++i) consider(ceil_slot(st.forced[i].at_ns), 1, i, st.forced[i].mode);
+      }
+      if (tid == 0) s_decide = INT_MAX;  // first fail-safe trip slot (scratch)
+      __syncthreads();
+      if (P.policy == ARCHES_POLICY_TREE && tid < len && !(decide && tid == len - 1) && !st.tripped &&
+          (n + 1) * slot_ns - st.last_delivery_ns > P.failsafe_timeout_ns && mode != 1)
+        atomicMin(&s_decide, tid);
+      __syncthreads();
+      const int trip = s_decide;  // INT_MAX: none
+      if (tid < len) {
+        if (trip != INT_MAX && tid > trip) consider(nbase + trip + 1, 1, ARCHES_MAX_PENDING, 1);
+        s_mode[tid] = mode;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        StreamState& sw = s_st;
+        const int64_t last = nbase + len - 1;
+        RegQueue pq, fq;
+        pq.load(sw.pending, sw.n_pending);
+        fq.load(sw.forced, sw.n_forced);
+        while (pq.n > 0 && ceil_slot(pq.at[0]) + (sel ? 1 : 0) <= last) pq.pop();
+        while (fq.n > 0 && ceil_slot(fq.at[0]) <= last) fq.pop();
+        int cnt = a.msg_count ? a.msg_count[stream] : 0;
+        if (trip != INT_MAX) {
+          const int64_t end_ns = (nbase + trip + 1) * slot_ns;
+          if (nbase + trip + 1 > last) fq.insert(end_ns, 1, ARCHES_TRIGGER_FAILSAFE);  // applies next chunk
+          sw.tripped = 1;
+          log_msg_fast(a.msg_log, a.msg_cap, stream, cnt, 1, end_ns, end_ns, ARCHES_TRIGGER_FAILSAFE);
+        }
+        pq.store(sw.pending, sw.n_pending);
+        fq.store(sw.forced, sw.n_forced);
+        sw.mode = s_mode[len - 1];
+        if (P.policy == ARCHES_POLICY_TREE) sw.since_decision += len;
+        if (a.msg_count) a.msg_count[stream] = cnt;
+        s_len = len;
+        s_decide = decide;
+      }
     } else if (tid == 0) {
       StreamState& st = s_st;
       RegQueue pq, fq;
