@@ -515,8 +515,10 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
       const int R = 2 * na * d.D, ncol = ((2 * R + 15) / 16) * 16, ng = ncol / 8;
       const int n_b = (ncol / 2) * 4 * d.tc_kb;  // B entries: <= 2 per thread of 512
       const int as = grp ? 4 : d.A;               // antennas per stage
-      const int nbuf = grp ? 2 : 3;  // B operands in flight (k2_tc NBUF)
-      sm = 2 * (size_t)(as + 1) * d.T * ARCHES_TILE * sizeof(float2) + 2 * nbuf * (size_t)d.tc_kb * ng * 256;
+      const int nbuf = 3;  // B operands in flight (k2_tc NBUF = LEAD + 1)
+      // two y (+ tx) stages; antenna groups keep the tile's tx rows in one extra buffer
+      sm = (2 * (size_t)(as + (grp ? 0 : 1)) + (grp ? 1 : 0)) * d.T * ARCHES_TILE * sizeof(float2) +
+           2 * nbuf * (size_t)d.tc_kb * ng * 256;
       if (grp) sm += (size_t)21 * TC_THREADS * sizeof(float);  // MRC sums across groups
       if (sm > 227 * 1024 || n_b > 2 * TC_THREADS || ncol > 64) sm = 0;
       // the per-tile phase rotations in shared memory when they fit

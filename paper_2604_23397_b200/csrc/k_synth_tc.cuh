@@ -355,8 +355,8 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
   constexpr int CPE = 2 * NA * ND;                  // D columns per expert
   // B operands / TMEM accumulators in flight: item i's MMA is issued as soon as
   // the epilogue of item i - LEAD is done, so its latency hides behind a whole
-  // epilogue (massive-MIMO plans keep one item of lead: shared memory)
-  constexpr int LEAD = kGrp ? 1 : 2;
+  // epilogue
+  constexpr int LEAD = 2;
   constexpr int NBUF = LEAD + 1;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t s_full[2];       // stage landed
@@ -383,10 +383,15 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
   const int lo = (int)((long long)blockIdx.x * n_titems / G) * ngrp;
   const int hi = (int)((long long)(blockIdx.x + 1) * n_titems / G) * ngrp;
   const uint32_t b_bytes = (uint32_t)KB * NG * 256;
-  const size_t stage_elems = (size_t)(AS + 1) * T * ARCHES_TILE;
+  // a stage holds the item's y rows and (one antenna group per item: massive
+  // MIMO) the tile's tx rows live in ONE buffer next to the stages: only a tile's
+  // last group reads them, and the load of the next tile's tx is issued after
+  // that item's equaliser finished (the stage refill rule below)
+  const size_t stage_elems = (size_t)(AS + (kGrp ? 0 : 1)) * T * ARCHES_TILE;
   const size_t coef_stride = coef_floats2(P);
   float2* sYX = reinterpret_cast<float2*>(sm);                               // [2][stage]
-  unsigned char* sB = sm + 2 * stage_elems * sizeof(float2);                 // [NBUF][hi | lo]
+  float2* sX = sYX + 2 * stage_elems;                                         // [T][TILE] (kGrp)
+  unsigned char* sB = sm + (2 * stage_elems + (kGrp ? (size_t)T * ARCHES_TILE : 0)) * sizeof(float2);
   float* gacc = reinterpret_cast<float*>(sB + 2 * NBUF * (size_t)KB * NG * 256) + threadIdx.x;  // [21][512] (kGrp)
   float2* srot = reinterpret_cast<float2*>(sB + 2 * NBUF * (size_t)KB * NG * 256);  // [n_tiles][L4+8] (!kGrp)
   const int n_all = (NCOL / 2) * L4;                                         // B entries
@@ -440,14 +445,14 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
     const uint64_t pol = l2_evict_first_policy();
     float2* dst = sYX + (size_t)stage * stage_elems;
     const bool with_x = gr == ngrp - 1;  // tx rows: needed by the last group only
+    float2* xdst = kGrp ? sX : dst + (size_t)AS * T * ARCHES_TILE;
     if constexpr (kTmap) {  // lane 0: two tensor copies (y rows of the group, tx rows)
       if (lane == 0) {
         const size_t ybytes = (size_t)AS * T * ARCHES_TILE * sizeof(float2);
-        mbar_arrive_expect_tx(&s_full[stage], (uint32_t)(with_x ? stage_elems * sizeof(float2) : ybytes));
+        const size_t xbytes = (size_t)T * ARCHES_TILE * sizeof(float2);
+        mbar_arrive_expect_tx(&s_full[stage], (uint32_t)(with_x ? ybytes + xbytes : ybytes));
         tma_load_3d(dst, &tm_y, tile * 2 * ARCHES_TILE, gr * AS * T, u, &s_full[stage], pol);
-        if (with_x)
-          tma_load_3d(dst + (size_t)AS * T * ARCHES_TILE, &tm_x, tile * 2 * ARCHES_TILE, 0, u,
-                      &s_full[stage], pol);
+        if (with_x) tma_load_3d(xdst, &tm_x, tile * 2 * ARCHES_TILE, 0, u, &s_full[stage], pol);
       }
     } else {  // one 1-D bulk copy per row, rows spread over the lanes
       const int k0 = tile * ARCHES_TILE;
@@ -456,9 +461,13 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       if (lane == 0) mbar_arrive_expect_tx(&s_full[stage], rowb * (uint32_t)rows);
       __syncwarp();
       for (int r = lane; r < rows; r += 32) {
-        const float2* src = (r < AS * T) ? args.y + ((size_t)u * P.A * T + (size_t)gr * AS * T + r) * P.N + k0
-                                         : args.tx + ((size_t)u * T + (r - AS * T)) * P.N + k0;
-        bulk_g2s(dst + (size_t)r * ARCHES_TILE, src, rowb, &s_full[stage], pol);
+        if (r < AS * T)
+          bulk_g2s(dst + (size_t)r * ARCHES_TILE,
+                   args.y + ((size_t)u * P.A * T + (size_t)gr * AS * T + r) * P.N + k0, rowb,
+                   &s_full[stage], pol);
+        else
+          bulk_g2s(xdst + (size_t)(r - AS * T) * ARCHES_TILE,
+                   args.tx + ((size_t)u * T + (r - AS * T)) * P.N + k0, rowb, &s_full[stage], pol);
       }
     }
   };
@@ -651,7 +660,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
     if (valid) {
       const float modd = (kk & 1) ? 1.f : 0.f;  // pilot REs: even k on DMRS symbols
       const float2* yrow = sYX + (size_t)buf * stage_elems + j;
-      const float2* xrow = yrow + (size_t)AS * T * ARCHES_TILE;
+      const float2* xrow = kGrp ? sX + j : yrow + (size_t)AS * T * ARCHES_TILE;
       if constexpr (kGrp) {  // antenna groups: MRC sums across the tile's groups, finalised at the last
         const bool first = gr == 0, last = gr + 1 == ngrp;
         if (half == 0) {
