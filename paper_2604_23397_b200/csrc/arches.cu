@@ -524,7 +524,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
       // the per-tile phase rotations in shared memory when they fit
       const size_t rot_bytes = (size_t)d.n_tiles * (4 * d.tc_kb + 8) * sizeof(float2);
       d.k2_rot_smem = 0;
-      if (sm && !grp && sm + rot_bytes <= 227 * 1024) {
+      if (sm && sm + rot_bytes <= 227 * 1024) {
         sm += rot_bytes;
         d.k2_rot_smem = 1;
       }

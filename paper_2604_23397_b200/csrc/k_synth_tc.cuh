@@ -393,7 +393,8 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
   float2* sX = sYX + 2 * stage_elems;                                         // [T][TILE] (kGrp)
   unsigned char* sB = sm + (2 * stage_elems + (kGrp ? (size_t)T * ARCHES_TILE : 0)) * sizeof(float2);
   float* gacc = reinterpret_cast<float*>(sB + 2 * NBUF * (size_t)KB * NG * 256) + threadIdx.x;  // [21][512] (kGrp)
-  float2* srot = reinterpret_cast<float2*>(sB + 2 * NBUF * (size_t)KB * NG * 256);  // [n_tiles][L4+8] (!kGrp)
+  float2* srot = reinterpret_cast<float2*>(sB + 2 * NBUF * (size_t)KB * NG * 256 +
+                                           (kGrp ? (size_t)21 * TC_THREADS * sizeof(float) : 0));  // [n_tiles][L4+8]
   const int n_all = (NCOL / 2) * L4;                                         // B entries
   const uint32_t ACC0 = 128;                                                 // TMEM columns
   // this thread's <= 2 B entries (output column pair r, tap l): source offsets
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
   // current item's epilogue
   auto load_b = [&](int u, int tile, int gr, float2 (&cv)[4]) {
     const float2* cu = args.coef + (size_t)u * coef_stride;
-    const bool rs = !kGrp && P.k2_rot_smem;
+    const bool rs = P.k2_rot_smem;
     const float2* rot = (rs ? srot : P.tc_rot) + (size_t)tile * (L4 + 8);
     const int bo = P.n_blocks == 1 ? 0 : min(tile * ARCHES_TILE / P.block, P.n_blocks - 1) * 8;
 #pragma unroll
@@ -557,7 +558,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
   }
-  if (!kGrp && P.k2_rot_smem && threadIdx.x < TC_THREADS)
+  if (P.k2_rot_smem && threadIdx.x < TC_THREADS)
     for (int i = threadIdx.x; i < n_tiles * (L4 + 8); i += TC_THREADS) srot[i] = __ldg(&P.tc_rot[i]);
   tc_fence_before();
   __syncthreads();
