@@ -670,7 +670,22 @@ static int launch_k1t(const arches_plan* P, int n_units, const GridCombSrc& src,
   k1_tc<48, 40><<<grid, K1T_THREADS, smem, s>>>(d, a, kg.n_items, tm[0], tm[1], tm[2], tm[3]);
   LAUNCH_CHECK();
   if (g_hook.before_fin) CUDA_TRY(cudaStreamWaitEvent(s, g_hook.before_fin, 0));
-  k1_tc_finalize<<<n_units, K1T_FIN_THREADS, 0, s>>>(d, a, n_units, o);
+  {
+    // programmatic dependent launch: the finalize's CTAs are scheduled while K1's
+    // last CTAs drain (launch latency off the critical path) and wait in-kernel
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(n_units);
+    cfg.blockDim = dim3(K1T_FIN_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, k1_tc_finalize, d, a, n_units, o));
+  }
   LAUNCH_CHECK();
   return ARCHES_OK;
 }

@@ -141,6 +141,9 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
         smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // the finalize (programmatic dependent launch) may be scheduled onto SMs as
+  // they free up; it waits for this grid's completion before reading anything
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -371,6 +374,8 @@ __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev 
                                                                  int n_units, K1Out o) {
   __shared__ double s_bins[4096];
   __shared__ double s_e[K1T_FIN_THREADS / 32], s_g[K1T_FIN_THREADS / 32];
+  // launched programmatically behind K1: wait for its grid (and its writes)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int u = blockIdx.x;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int L = P.L, ncol = 2 * L, AD = P.A * P.D, nout = AD * ncol;
