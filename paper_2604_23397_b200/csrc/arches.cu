@@ -810,6 +810,25 @@ static bool make_row_tmap(CUtensorMap* m, const void* base, int N, int rows, int
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// launch with programmatic stream serialization: the kernel may start while the
+// previous kernel of the stream drains and synchronises with griddepcontrol.wait
+template <typename K, typename... Args>
+static cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cudaStream_t s) {
   const PlanDev& d = P->dev;
   const int ngrp = P->k2_groups;
@@ -828,7 +847,7 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
   {                                                                                          \
     auto kern = tmap ? k2_tc<NA_, ND_, STD_, true, GRP_> : k2_tc<NA_, ND_, STD_, false, GRP_>; \
     CUDA_TRY(ensure_smem(kern, smem));                                                       \
-    kern<<<grid, TC_BLOCK, smem, s>>>(d, a, n_items, tm_y, tm_x);                            \
+    CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(TC_BLOCK), smem, s, d, a, n_items, tm_y, tm_x)); \
     LAUNCH_CHECK();                                                                          \
     /* K3 locates the (CTA, unit) segments in tile units */                                  \
     cudaStream_t s3 = s;                                                                     \

@@ -374,8 +374,10 @@ __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev 
                                                                  int n_units, K1Out o) {
   __shared__ double s_bins[4096];
   __shared__ double s_e[K1T_FIN_THREADS / 32], s_g[K1T_FIN_THREADS / 32];
-  // launched programmatically behind K1: wait for its grid (and its writes)
+  // launched programmatically behind K1: wait for its grid (and its writes); K2
+  // may then be scheduled as this grid drains
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int u = blockIdx.x;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int L = P.L, ncol = 2 * L, AD = P.A * P.D, nout = AD * ncol;

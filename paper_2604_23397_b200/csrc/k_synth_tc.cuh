@@ -585,6 +585,10 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       }
     }
   } else {
+  // programmatic dependent launch behind the K1 finalize: the prologue above (TMEM,
+  // twiddle operand, phase table) and the producer's y / tx loads overlap its tail;
+  // the coefficients it writes are read only after its grid completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (lo < hi) {  // B of the first LEAD items
     int bu = u, bt = tile, bg = gr;
     for (int k = 0; k < LEAD && k < count; ++k) {
