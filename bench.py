@@ -642,6 +642,11 @@ def run_policy_stress(a, rank, world, backend):
     torch.cuda.synchronize()
     clocks = ClockSampler(physical_gpu(torch))
     clocks.start()
+    t_end = time.time() + 1.0   # sustained load so the sampler sees the clocks under load
+    while time.time() < t_end:
+        for _ in range(20):
+            g.replay()
+        torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
