@@ -668,21 +668,13 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       const float2* xrow = kGrp ? sX + j : yrow + (size_t)AS * T * ARCHES_TILE;
       if constexpr (kGrp) {  // antenna groups: MRC sums across the tile's groups, finalised at the last
         const bool first = gr == 0, last = gr + 1 == ngrp;
-        if (half == 0) {
-          if (ex == 0) eq_grp_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
-          else         eq_grp_half<NA, ND, 0, false>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
-        } else {
-          if (ex == 0) eq_grp_half<NA, ND, 1, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
-          else         eq_grp_half<NA, ND, 1, false>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
-        }
+        // |x|^2 is accumulated by both experts' threads (only expert 0's is reduced):
+        // one instantiation per half keeps the loop body in the instruction cache
+        if (half == 0) eq_grp_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
+        else           eq_grp_half<NA, ND, 1, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
       } else if constexpr (kStd) {  // compile-time symbol half and expert: weights and pilot symbols fold
-        if (half == 0) {
-          if (ex == 0) eq_std_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
-          else         eq_std_half<NA, ND, 0, false>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
-        } else {
-          if (ex == 0) eq_std_half<NA, ND, 1, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
-          else         eq_std_half<NA, ND, 1, false>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
-        }
+        if (half == 0) eq_std_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
+        else           eq_std_half<NA, ND, 1, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
       } else {
         const int t0 = half ? TH : 0, t1 = half ? T : TH;
         for (int t = t0; t < t1; ++t) {
