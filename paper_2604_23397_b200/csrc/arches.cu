@@ -847,7 +847,7 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
   {                                                                                          \
     auto kern = tmap ? k2_tc<NA_, ND_, STD_, true, GRP_> : k2_tc<NA_, ND_, STD_, false, GRP_>; \
     CUDA_TRY(ensure_smem(kern, smem));                                                       \
-    CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(TC_BLOCK), smem, s, d, a, n_items, tm_y, tm_x)); \
+    CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(GRP_ ? TC_THREADS : TC_BLOCK), smem, s, d, a, n_items, tm_y, tm_x)); \
     LAUNCH_CHECK();                                                                          \
     /* K3 locates the (CTA, unit) segments in tile units */                                  \
     cudaStream_t s3 = s;                                                                     \

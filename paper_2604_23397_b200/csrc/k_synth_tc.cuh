@@ -23,7 +23,7 @@
 #include "k_synth_eq.cuh"
 
 #define TC_THREADS 512                   // epilogue threads: 128 subcarriers x 2 experts x 2 symbol halves
-#define TC_BLOCK (TC_THREADS + 32)       // + the producer / MMA warp
+#define TC_BLOCK (TC_THREADS + 32)       // + the producer / MMA warp (single-group plans)
 
 __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   // SWIZZLE_NONE K-major canonical layout: core matrices of 8 rows x 16 B,
@@ -346,7 +346,7 @@ __device__ __forceinline__ void eq_grp_half(const float2 (&h)[NA][ND], const flo
 }
 
 template <int NA, int ND, bool kStd, bool kTmap, bool kGrp = false>
-__global__ void __launch_bounds__(TC_BLOCK, 1)
+__global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
     k2_tc(const PlanDev P, const K2Args args, const int n_items,
           const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ CUtensorMap tm_x) {
   constexpr int R = 2 * NA * ND;                    // complex outputs: AI then MMSE
@@ -358,10 +358,15 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
   // epilogue
   constexpr int LEAD = 2;
   constexpr int NBUF = LEAD + 1;
+  // single-group plans: a producer warp issues the MMAs and stage refills.
+  // Antenna-group plans (longer epilogue, 96 registers would spill under a 17th
+  // warp): the last epilogue warp to complete a B operand issues them itself
+  constexpr bool kProd = !kGrp;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t s_full[2];       // stage landed
   __shared__ __align__(8) uint64_t s_mma[NBUF];     // accumulator ready
-  __shared__ __align__(8) uint64_t s_bready[NBUF];  // B(i) written (512 arrivals)
+  __shared__ __align__(8) uint64_t s_bready[NBUF];  // B(i) written (512 arrivals; kProd)
+  __shared__ uint32_t s_bcount[NBUF];               // B(i) writers arrived, +32 per warp (!kProd)
   __shared__ uint32_t s_tmem;
   __shared__ double s_red[2][11][8];
   const int KB = P.tc_kb, L4 = 4 * KB;
@@ -429,6 +434,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&s_mma[b], 1);
       mbar_init(&s_bready[b], TC_THREADS);
+      s_bcount[b] = 0;
     }
   }
   if (warp == 0) {
@@ -502,7 +508,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   };
-  auto issue_mma = [&](int buf) {  // producer warp lane 0, once B(buf) is written
+  auto issue_mma = [&](int buf) {  // lane 0 of the producer (or completing) warp, once B(buf) is written
     tc_fence_after();
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NCOL >> 3) << 17) |
                            ((uint32_t)(ARCHES_TILE >> 4) << 24);
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
   __syncthreads();
   tc_fence_after();
 
-  if (warp == TC_THREADS / 32) {
+  if (kProd && warp == TC_THREADS / 32) {
     // ---------------- producer / MMA warp.  B(j) written means the epilogue of
     // item j - LEAD is finished: MMA(j) goes out (its accumulator was read by
     // item j - NBUF), and the stage item j - LEAD used is refilled with item
@@ -585,6 +591,37 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       }
     }
   } else {
+  if (!kProd && warp == 0) {  // the first two items' y / tx rows
+    int tu = u, tt = tile, tg = gr;
+    for (int k = 0; k < 2 && k < count; ++k) {
+      issue_tma(tu, tt, tg, k);
+      advance(tu, tt, tg);
+    }
+  }
+  // B(jj) of item (bu, bt, bg) written by this thread.  !kProd: the warp arrives
+  // on the buffer's counter and the last of the 16 warps issues MMA(jj) (its
+  // accumulator was read by item jj - NBUF, whose readers have all arrived) and
+  // refills the stage item jj - LEAD used with item jj; no warp waits
+  auto arrive_b = [&](int jj, int bu, int bt, int bg) {
+    tc_fence_before();
+    if constexpr (kProd) {
+      mbar_arrive(&s_bready[jj % NBUF]);
+    } else {
+      __syncwarp();
+      uint32_t old = 0;
+      if (lane == 0)
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 32;"
+                     : "=r"(old)
+                     : "r"(smem_u32(&s_bcount[jj % NBUF]))
+                     : "memory");
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (((old + 32u) & (TC_THREADS - 1)) == 0) {
+        if (lane == 0) issue_mma(jj % NBUF);
+        __syncwarp();
+        if (jj >= 2 && jj < count) issue_tma(bu, bt, bg, jj & 1);
+      }
+    }
+  };
   // programmatic dependent launch behind the K1 finalize: the prologue above (TMEM,
   // twiddle operand, phase table) and the producer's y / tx loads overlap its tail;
   // the coefficients it writes are read only after its grid completed
@@ -595,8 +632,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
       float2 cv[4];
       load_b(bu, bt, bg, cv);
       write_b(k, cv);
-      tc_fence_before();
-      mbar_arrive(&s_bready[k]);
+      arrive_b(k, bu, bt, bg);
       advance(bu, bt, bg);
     }
   }
@@ -719,8 +755,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1)
     // ---- B(i + LEAD) -> shared memory; signals the producer / MMA warp
     if (has_lead) {
       write_b((i + LEAD) % NBUF, cv);
-      tc_fence_before();
-      mbar_arrive(&s_bready[(i + LEAD) % NBUF]);
+      arrive_b(i + LEAD, lu, lt, lg);
     }
     // ---- segment partial (fixed order); per-unit finalisation runs in K3
     if (flush && warp == 1 && lane < 11) {
