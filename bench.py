@@ -568,7 +568,7 @@ def run_ours(a, rank, world, backend):
                            "noise_var + regime -> H2D -> unpack + run (graph) -> D2H KPM records, "
                            "every step, one stream"},
             "latency": lat,
-            "gpu_launches": 6 * K,  # RNG, K1, K1 finalize, K2, K3, K4 per step
+            "gpu_launches": plan.batch_kernels() * K,  # RNG, K1, K1 finalize(s), K2, K3, K4 per step
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -270,6 +270,11 @@ int arches_run_batch_async(const arches_plan* plan, int32_t n_streams, int32_t n
  * (no-op when none is pending). */
 int arches_join(const arches_plan* plan, arches_stream_t stream);
 
+/* Number of kernels one arches_run_batch / arches_run_batch_async call launches
+ * for this plan (RNG, K1, the K1 finalize grid(s), K2, K3, K4; memsets and
+ * event records not counted).  Benchmarks report it; no reference counterpart. */
+int32_t arches_batch_kernels(const arches_plan* plan);
+
 /* ---- K5: zero-gap switch, reference aliasing semantics ---------------
  * switch_select (phy_pipeline.py:81-91): for every unit whose kpm.mode == 1
  * copy the MMSE output into the AI (downstream) buffer; mode 0 is a no-op. */

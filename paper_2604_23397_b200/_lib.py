@@ -84,6 +84,7 @@ _SIGS = {
     "arches_plan_destroy": (C.c_int, [P]),
     "arches_state_bytes": (C.c_size_t, [P, C.c_int32]),
     "arches_workspace_bytes": (C.c_size_t, [P, C.c_int32]),
+    "arches_batch_kernels": (C.c_int32, [P]),
     "arches_state_init": (C.c_int, [P, P, C.c_int32, P]),
     "arches_ls_analyze": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, C.c_int64, P, P, P, P]),
     "arches_experts_equalize": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, P, C.c_int64, P, P,

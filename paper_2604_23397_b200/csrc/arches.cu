@@ -119,7 +119,7 @@ static cudaError_t ensure_smem(K kern, size_t smem) {
 
 // ------------------------------------------------------------ workspace
 struct WsLayout {
-  size_t coef, parts, counters, k1parts, k1counters, sigma2, rng, k1t_d, k1t_e, total;
+  size_t coef, parts, counters, k1parts, k1counters, sigma2, rng, k1t_d, k1t_e, k1t_share, total;
 };
 
 // tensor-core K1 work split: 128-row tiles x DMRS symbols x subcarrier parts,
@@ -128,6 +128,13 @@ struct K1TGeom {
   int n_g, parts, cpp, n_items;
 };
 static K1TGeom k1t_geom(const arches_plan* P, int n_units);
+
+// row chunks of the tensor-core K1 finalize: 1 (one CTA per unit, bins staged in
+// shared memory) unless a unit's bins exceed that stage
+static int k1t_fin_chunks(const PlanDev& d) {
+  const int AD = d.A * d.D;
+  return AD * 2 * d.L <= 4096 ? 1 : (AD + K1T_FIN_ROWS - 1) / K1T_FIN_ROWS;
+}
 
 static WsLayout ws_layout(const arches_plan* P, int n_units) {
   const PlanDev& d = P->dev;
@@ -150,13 +157,15 @@ static WsLayout ws_layout(const arches_plan* P, int n_units) {
   off += align256((size_t)n_units * sizeof(double));
   w.rng = off;
   off += align256((size_t)n_units * 2 * sizeof(double));
-  w.k1t_d = w.k1t_e = off;
+  w.k1t_d = w.k1t_e = w.k1t_share = off;
   if (P->k1t_nb) {
     const K1TGeom kg = k1t_geom(P, n_units);
     w.k1t_d = off;
     off += align256((size_t)kg.n_items * 128 * 2 * d.L * sizeof(double));
     w.k1t_e = off;
     off += align256((size_t)kg.n_items * 128 * sizeof(double));
+    w.k1t_share = off;  // row-chunked finalize: per-CTA energy / guard shares
+    off += align256((size_t)n_units * k1t_fin_chunks(d) * 2 * sizeof(double));
   }
   w.total = off;
   return w;
@@ -666,6 +675,7 @@ static int launch_k1t(const arches_plan* P, int n_units, const GridCombSrc& src,
       return set_err(ARCHES_E_CUDA, "K1: tensor map encode failed");
   const int grid = std::min(kg.n_items, d.num_sms);
   const size_t smem = k1t_smem_bytes(a.nb);
+  const int nchunk = k1t_fin_chunks(d);
   CUDA_TRY(ensure_smem(k1_tc<48, 40>, smem));
   k1_tc<48, 40><<<grid, K1T_THREADS, smem, s>>>(d, a, kg.n_items, tm[0], tm[1], tm[2], tm[3]);
   LAUNCH_CHECK();
@@ -675,7 +685,7 @@ static int launch_k1t(const arches_plan* P, int n_units, const GridCombSrc& src,
     // last CTAs drain (launch latency off the critical path) and wait in-kernel
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3(n_units);
+    cfg.gridDim = dim3(n_units * nchunk);
     cfg.blockDim = dim3(K1T_FIN_THREADS);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
@@ -684,7 +694,15 @@ static int launch_k1t(const arches_plan* P, int n_units, const GridCombSrc& src,
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, k1_tc_finalize, d, a, n_units, o));
+    if (nchunk > 1) {
+      CUDA_TRY(cudaLaunchKernelEx(&cfg, k1_tc_finalize_rows, d, a, nchunk, o,
+                                  ws_at<double>(ws, w.k1t_share)));
+      LAUNCH_CHECK();
+      cfg.blockDim = dim3(K1T_FIN_ROWS * 32);
+      CUDA_TRY(cudaLaunchKernelEx(&cfg, k1_tc_finalize_taps, d, nchunk, o,
+                                  static_cast<const double*>(ws_at<double>(ws, w.k1t_share))));
+    } else
+      CUDA_TRY(cudaLaunchKernelEx(&cfg, k1_tc_finalize, d, a, n_units, o));
   }
   LAUNCH_CHECK();
   return ARCHES_OK;
@@ -921,6 +939,13 @@ static int experts_equalize_impl(const arches_plan* plan, int32_t n_streams, int
   a.rng = rng_from_k1 ? ws_at<double>(ws, w.rng) : nullptr;
   if (plan->k2_tc_smem) return launch_k2_tc(plan, n_units, a, s);
   return launch_k2<2>(plan, n_units, a, s);
+}
+
+extern "C" int32_t arches_batch_kernels(const arches_plan* plan) {
+  if (!plan) return 0;
+  const int k1 = plan->k1t_nb ? 1 + (k1t_fin_chunks(plan->dev) > 1 ? 2 : 1) : 1;
+  const int k2 = plan->k2_tc_smem ? 2 : 1;  // tensor-core K2 + K3, or the FFMA form
+  return 1 + k1 + k2 + 1;                    // + RNG, K4
 }
 
 // ------------------------------------------------------------ K4 / K5

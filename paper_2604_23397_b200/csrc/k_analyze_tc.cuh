@@ -443,3 +443,101 @@ __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev 
     ca[o2] = make_float2((float)c.x, (float)c.y);
   }
 }
+
+// Many-antenna plans (A*D*2L bins > the 4096 the per-unit finalize stages in
+// shared memory): the same arithmetic in two programmatically chained grids of
+// (unit, K1T_FIN_ROWS (a, d) rows) CTAs, so a handful of units still fill the
+// SMs.  Rows: each CTA sums its rows' parts into the unit's bins (global
+// scratch) and its share of the row energy / guard power.  Taps: each CTA sums
+// the unit's shares in chunk order (every CTA of a unit forms the same sigma2)
+// and writes its rows' MMSE / AI taps.
+#define K1T_FIN_ROWS 16
+__global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize_rows(const PlanDev P, const K1TArgs a,
+                                                                      int nchunk, K1Out o,
+                                                                      double* share /*[u][nchunk][2]*/) {
+  __shared__ double s_e[K1T_FIN_THREADS / 32], s_g[K1T_FIN_THREADS / 32];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int u = blockIdx.x / nchunk, c = blockIdx.x - u * nchunk;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int L = P.L, ncol = 2 * L, AD = P.A * P.D;
+  const int r0 = c * K1T_FIN_ROWS, r1 = min(AD, r0 + K1T_FIN_ROWS);
+  double* acc = o.parts + (size_t)u * (2 * (size_t)AD * L + 2);
+  const int np = a.parts;
+  const size_t pstride = (size_t)P.D * a.n_g * 128 * ncol;
+  double sg = 0.0;
+  for (int o2 = r0 * ncol + tid; o2 < r1 * ncol; o2 += K1T_FIN_THREADS) {
+    const int ad = o2 / ncol, cc = o2 - ad * ncol;
+    const int aa = ad / P.D, d = ad - aa * P.D;
+    const int row = u * P.A + aa, g = row / 128, r = row - g * 128;
+    const double* src = a.dpart + ((size_t)(d * a.n_g + g) * 128 + r) * ncol + cc;
+    double sum = 0.0;
+    for (int q0 = 0; q0 < np; q0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = q0 + k < np ? __ldcg(src + (size_t)(q0 + k) * pstride) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += v[k];
+    }
+    __stcg(&acc[o2], sum);
+    if (cc < 2 * P.guard) sg += sum * sum;
+  }
+  double e = 0.0;
+  for (int o2 = tid; o2 < (r1 - r0) * np; o2 += K1T_FIN_THREADS) {
+    const int ad = r0 + o2 / np, q = o2 % np;
+    const int aa = ad / P.D, d = ad - aa * P.D;
+    const int row = u * P.A + aa, g = row / 128, r = row - g * 128;
+    e += __ldcg(a.epart + (size_t)((q * P.D + d) * a.n_g + g) * 128 + r);
+  }
+  e = warp_sum(e);
+  sg = warp_sum(sg);
+  if (lane == 0) {
+    s_e[w] = e;
+    s_g[w] = sg;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double et = 0.0, gt = 0.0;
+#pragma unroll
+    for (int k = 0; k < K1T_FIN_THREADS / 32; ++k) {
+      et += s_e[k];
+      gt += s_g[k];
+    }
+    __stcg(&share[((size_t)u * nchunk + c) * 2], et);
+    __stcg(&share[((size_t)u * nchunk + c) * 2 + 1], gt);
+  }
+}
+
+__global__ void __launch_bounds__(K1T_FIN_ROWS * 32) k1_tc_finalize_taps(const PlanDev P, int nchunk,
+                                                                        K1Out o, const double* share) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int u = blockIdx.x / nchunk, c = blockIdx.x - u * nchunk;
+  const int tid = threadIdx.x;
+  const int L = P.L, ncol = 2 * L, AD = P.A * P.D;
+  const int r0 = c * K1T_FIN_ROWS, r1 = min(AD, r0 + K1T_FIN_ROWS);
+  const double* acc = o.parts + (size_t)u * (2 * (size_t)AD * L + 2);
+  double et = 0.0, gt = 0.0;
+  for (int k = 0; k < nchunk; ++k) {
+    et += __ldcg(&share[((size_t)u * nchunk + k) * 2]);
+    gt += __ldcg(&share[((size_t)u * nchunk + k) * 2 + 1]);
+  }
+  const double nvhat = (et - gt / (double)P.M) / ((double)AD * (P.M - P.guard));
+  if (c == 0 && tid == 0 && o.sigma2) o.sigma2[u] = nvhat;
+  const double sgm = nvhat + P.ridge;
+  const int M = P.M;
+  float2* cm = o.coef + (size_t)u * coef_floats2(P);
+  float2* ca = cm + (size_t)AD * 8;
+  for (int o2 = r0 * 8 + tid; o2 < r1 * 8; o2 += K1T_FIN_ROWS * 32) {
+    const int ad = o2 >> 3, l = o2 & 7;
+    const double wl = P.pdp[l] / ((double)M * P.pdp[l] + sgm);
+    cm[o2] = make_float2((float)(wl * __ldcg(&acc[ad * ncol + 2 * l])),
+                         (float)(wl * __ldcg(&acc[ad * ncol + 2 * l + 1])));
+  }
+  for (int o2 = r0 * P.trunc + tid; o2 < r1 * P.trunc; o2 += K1T_FIN_ROWS * 32) {
+    const int ad = o2 / P.trunc, l = o2 - ad * P.trunc;
+    const double2 bb = make_double2(__ldcg(&acc[ad * ncol + 2 * l]), __ldcg(&acc[ad * ncol + 2 * l + 1]));
+    const double2 cz = zmul(P.ai_fac[l], bb);
+    ca[o2] = make_float2((float)cz.x, (float)cz.y);
+  }
+}

@@ -105,6 +105,10 @@ class ArchesPlan:
     def workspace_bytes(self, n_units: int) -> int:
         return _lib.lib().arches_workspace_bytes(self.handle, n_units)
 
+    def batch_kernels(self) -> int:
+        """Kernels one run_batch call launches for this plan (arches_batch_kernels)."""
+        return int(_lib.lib().arches_batch_kernels(self.handle))
+
     def close(self):
         if getattr(self, "handle", None):
             _lib.lib().arches_plan_destroy(self.handle)

@@ -57,3 +57,16 @@ def test_massive_mimo_layers_match_oracle(n_prb, n_ant, n_layers, n_slots):
                                   f"layer {k} slot {i} mmse")
             assert_estimate_close(to_ref_layout(eng.h_ai[u].cpu().numpy()), sr.ai,
                                   f"layer {k} slot {i} ai")
+
+
+def test_batch_kernel_counts():
+    """arches_batch_kernels (the count bench.py reports): RNG + K1 + finalize
+    grid(s) + K2 + K3 + K4; many-antenna plans finalise in two grids (rows, taps);
+    the CUDA-core forms finalise in line."""
+    from paper_2604_23397_b200.engine import ArchesPlan
+    pcfg = PipelineConfig()
+    geo_b, geo_e = SlotGeometry(n_ant=4, n_prb=273), SlotGeometry(n_ant=64, n_prb=273)
+    assert ArchesPlan(geo_b, 1.25, pcfg, ExecutionMode.CONCURRENT, "oracle").batch_kernels() == 6
+    assert ArchesPlan(geo_e, 1.25, pcfg, ExecutionMode.CONCURRENT, "oracle").batch_kernels() == 7
+    assert ArchesPlan(geo_b, 1.25, pcfg, ExecutionMode.CONCURRENT, "oracle",
+                      flags=0x3).batch_kernels() == 4

@@ -39,7 +39,8 @@ def main():
 
     for geo, flags, em in ((SlotGeometry(n_ant=4, n_prb=24), 0, ExecutionMode.CONCURRENT),
                            (SlotGeometry(n_ant=4, n_prb=12), 0x3, ExecutionMode.SELECTED_ONLY),
-                           (SlotGeometry(n_ant=16, n_prb=12), 0, ExecutionMode.CONCURRENT)):
+                           (SlotGeometry(n_ant=16, n_prb=12), 0, ExecutionMode.CONCURRENT),
+                           (SlotGeometry(n_ant=64, n_prb=12), 0, ExecutionMode.CONCURRENT)):
         eng = engine(geo, 2, 6, flags, em)
         eng.run()                         # sequential executor (RNG forked on the side stream)
         for _ in range(3):
