@@ -517,10 +517,18 @@ __global__ void __launch_bounds__(K1T_FIN_ROWS * 32) k1_tc_finalize_taps(const P
   const int L = P.L, ncol = 2 * L, AD = P.A * P.D;
   const int r0 = c * K1T_FIN_ROWS, r1 = min(AD, r0 + K1T_FIN_ROWS);
   const double* acc = o.parts + (size_t)u * (2 * (size_t)AD * L + 2);
+  // the unit's shares: 32 in flight per warp (one per lane), summed in chunk
+  // order through shuffles -- every warp of every CTA of the unit gets the same
   double et = 0.0, gt = 0.0;
-  for (int k = 0; k < nchunk; ++k) {
-    et += __ldcg(&share[((size_t)u * nchunk + k) * 2]);
-    gt += __ldcg(&share[((size_t)u * nchunk + k) * 2 + 1]);
+  const int lane = tid & 31;
+  for (int k0 = 0; k0 < nchunk; k0 += 32) {
+    const bool have = k0 + lane < nchunk;
+    const double ve = have ? __ldcg(&share[((size_t)u * nchunk + k0 + lane) * 2]) : 0.0;
+    const double vg = have ? __ldcg(&share[((size_t)u * nchunk + k0 + lane) * 2 + 1]) : 0.0;
+    for (int k = 0; k < 32 && k0 + k < nchunk; ++k) {
+      et += __shfl_sync(0xffffffffu, ve, k);
+      gt += __shfl_sync(0xffffffffu, vg, k);
+    }
   }
   const double nvhat = (et - gt / (double)P.M) / ((double)AD * (P.M - P.guard));
   if (c == 0 && tid == 0 && o.sigma2) o.sigma2[u] = nvhat;
