@@ -365,8 +365,8 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t s_full[2];       // stage landed
   __shared__ __align__(8) uint64_t s_mma[NBUF];     // accumulator ready
-  __shared__ __align__(8) uint64_t s_bready[NBUF];  // B(i) written (512 arrivals; kProd)
-  __shared__ uint32_t s_bcount[NBUF];               // B(i) writers arrived, +32 per warp (!kProd)
+  __shared__ __align__(8) uint64_t s_bready[NBUF];  // B(i) written (512 thread / 16 warp arrivals)
+  __shared__ uint32_t s_bcount[NBUF];               // warps arrived on B(i) (!kProd: elects the issuer)
   __shared__ uint32_t s_tmem;
   __shared__ double s_red[2][11][8];
   const int KB = P.tc_kb, L4 = 4 * KB;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
     mbar_init(&s_full[1], 1);
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&s_mma[b], 1);
-      mbar_init(&s_bready[b], TC_THREADS);
+      mbar_init(&s_bready[b], kProd ? TC_THREADS : TC_THREADS / 32);
       s_bcount[b] = 0;
     }
   }
@@ -598,10 +598,11 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
       advance(tu, tt, tg);
     }
   }
-  // B(jj) of item (bu, bt, bg) written by this thread.  !kProd: the warp arrives
-  // on the buffer's counter and the last of the 16 warps issues MMA(jj) (its
-  // accumulator was read by item jj - NBUF, whose readers have all arrived) and
-  // refills the stage item jj - LEAD used with item jj; no warp waits
+  // B(jj) of item (bu, bt, bg) written by this thread.  !kProd: each warp arrives
+  // on the buffer's mbarrier (release) and bumps a relaxed counter that elects
+  // the 16th warp, which waits for the phase (acquire, completes at once) and
+  // issues MMA(jj) (its accumulator was read by item jj - NBUF, whose readers
+  // have all arrived) and the refill of the stage item jj - LEAD used
   auto arrive_b = [&](int jj, int bu, int bt, int bg) {
     tc_fence_before();
     if constexpr (kProd) {
@@ -609,13 +610,13 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
     } else {
       __syncwarp();
       uint32_t old = 0;
-      if (lane == 0)
-        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 32;"
-                     : "=r"(old)
-                     : "r"(smem_u32(&s_bcount[jj % NBUF]))
-                     : "memory");
+      if (lane == 0) {
+        mbar_arrive(&s_bready[jj % NBUF]);
+        old = atomicAdd(&s_bcount[jj % NBUF], 1u);
+      }
       old = __shfl_sync(0xffffffffu, old, 0);
-      if (((old + 32u) & (TC_THREADS - 1)) == 0) {
+      if ((old & (TC_THREADS / 32 - 1)) == TC_THREADS / 32 - 1) {
+        mbar_wait_spin(&s_bready[jj % NBUF], (jj / NBUF) & 1);
         if (lane == 0) issue_mma(jj % NBUF);
         __syncwarp();
         if (jj >= 2 && jj < count) issue_tma(bu, bt, bg, jj & 1);
