@@ -445,11 +445,12 @@ def run_ours(a, rank, world, backend):
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "k2_dram_traffic.json")
     if os.path.exists(tpath):  # dram__bytes_read + write per K2 launch, from a committed ncu capture
-        tj = json.load(open(tpath))
-        if tj.get("n_prb") == a.n_prb and tj.get("n_ant") == A and tj.get("units") == U:
-            traffic = tj["bytes_per_launch"]
-            traffic_src = (f"committed ncu --set full capture ({os.path.relpath(tpath, ROOT)}, "
-                           f"{tj.get('captured', 'this config')}), not measured in this run")
+        entries = json.load(open(tpath))
+        for tj in entries if isinstance(entries, list) else [entries]:
+            if tj.get("n_prb") == a.n_prb and tj.get("n_ant") == A and tj.get("units") == U:
+                traffic = tj["bytes_per_launch"]
+                traffic_src = (f"committed ncu capture ({os.path.relpath(tpath, ROOT)}, "
+                               f"{tj.get('captured', 'this config')}), not measured in this run")
 
     # ---- e2e through the public engine API: pinned host inputs -> H2D -> run -> D2H KPMs.
     # Pinned buffers are placed on the GPU's NUMA node (first touch by a thread
