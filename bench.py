@@ -73,6 +73,9 @@ def parse(argv=None):
     ap.add_argument("--mode", default="pipeline", choices=["pipeline", "policy-stress"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--latency-slots", type=int, default=400)
+    ap.add_argument("--tx", default="complex", choices=["packed", "complex"],
+                    help="resident genie-tx format: the complex64 grid, or 2-bit QPSK codes read "
+                         "by K2 (ARCHES_FLAG_TX_PACKED, n_ant 1/2/4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sequential", action="store_true",
                     help="one CUDA graph per step, no cross-batch pipeline (arches_run_batch)")
@@ -351,8 +354,10 @@ def run_ours(a, rank, world, backend):
     geo, scens, pil, y, tx, nv, reg = make_stream_inputs(a.n_prb, a.n_ant, S, seeds)
     A, T, N, D = geo.n_ant, geo.n_sym, geo.n_sc, geo.n_dmrs
     tree = from_text(open(a.tree).read()) if a.policy == "tree" else None
+    # --tx packed: tx resident as the packed QPSK wire format K2 reads (n_ant 1, 2, 4)
+    packed = a.tx == "packed" and A in (1, 2, 4)
     plan = ArchesPlan(geo, scens["good"].assumed_delay_spread, PipelineConfig(),
-                      ExecutionMode.CONCURRENT, a.policy)
+                      ExecutionMode.CONCURRENT, a.policy, flags=_lib.FLAG_TX_PACKED if packed else 0)
     eng = SlotEngine(plan, C, S, tree=tree)
     eng.set_streams(pil, seeds)
     eng.load(y=y, tx=tx, noise_var=nv, regime=reg)
@@ -433,8 +438,10 @@ def run_ours(a, rank, world, backend):
     k2 = np.mean([ev[4 * r + 1].elapsed_time(ev[4 * r + 2]) for r in range(reps)])
     k4 = np.mean([ev[4 * r + 2].elapsed_time(ev[4 * r + 3]) for r in range(reps)])
     # algorithmic bytes per unit: y read once (8 A T N), both experts written
-    # (2 x 8 A D N), the complex64 genie tx read once (8 T N) = 8 N (20 A + 14)
-    unit_bytes = 8 * N * (A * (T + 2 * D) + T)
+    # (2 x 8 A D N), the genie tx read once: 2-bit codes (n_tiles T 32 B) when
+    # packed, else the complex64 grid (8 T N) = 8 N (20 A + 14)
+    tx_bytes = -(-N // 128) * T * 32 if packed else 8 * T * N
+    unit_bytes = 8 * N * A * (T + 2 * D) + tx_bytes
     pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(pk_path)) if os.path.exists(pk_path) else {"hbm_gbs": 6650.0}
     peak = float(peaks["hbm_gbs"])
@@ -545,6 +552,8 @@ def run_ours(a, rank, world, backend):
             "data": "synthetic (reference TDL scene, bit-exact; S-slot pool per stream replayed each step)",
             "config": workload(a, world),
             "units_per_step": units // K, "streams_per_rank": C,
+            "tx_format": ("packed QPSK codes (2 bits/RE) read by K2" if packed
+                          else "complex64 grid"),
             "l2": f"inputs {U * unit_bytes / 1e6:.0f} MB per step per GPU vs 126 MB L2 "
                   f"({'> L2, no flush' if U * unit_bytes > 126e6 else '< L2: NOT L2-cold'})",
             "executor": ("cross-batch pipeline: step n's RNG/K3/K4 overlap step n+1's K1 "
@@ -566,8 +575,8 @@ def run_ours(a, rank, world, backend):
             "e2e": {"value": e2e_units / (te / 1000.0), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "how": "pinned host y (complex64) + tx (packed QPSK wire format, 2 bits/RE) + "
-                           "noise_var + regime -> H2D -> unpack + run (graph) -> D2H KPM records, "
-                           "every step, one stream"},
+                           "noise_var + regime -> H2D -> " + ("" if packed else "unpack + ") +
+                           "run (graph) -> D2H KPM records, every step, one stream"},
             "latency": lat,
             "gpu_launches": plan.batch_kernels() * K,  # RNG, K1, K1 finalize(s), K2, K3, K4 per step
             "clocks": clk,

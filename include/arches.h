@@ -61,6 +61,12 @@ typedef struct CUstream_st* arches_stream_t; /* == cudaStream_t */
  * tensor-core ones) */
 #define ARCHES_FLAG_NO_TC_K1 0x1 /* K1: CUDA-core comb analysis instead of tcgen05 */
 #define ARCHES_FLAG_NO_TC_K2 0x2 /* K2: FFMA synthesis/equaliser instead of tcgen05 */
+/* the `tx` argument of arches_run_batch / arches_run_batch_async /
+ * arches_experts_equalize / arches_perturb_mmse is the packed QPSK wire format
+ * ([u][n_tiles][T][32] bytes, arches_pack_qpsk) instead of the complex64 grid:
+ * K2 reads 2 bits per RE (results identical).  Requires the tensor-core K2 over
+ * one antenna group with the NR 0/5/10 DMRS pattern (n_ant 1, 2 or 4). */
+#define ARCHES_FLAG_TX_PACKED 0x4
 
 enum { ARCHES_EXEC_CONCURRENT = 0, ARCHES_EXEC_SELECTED_ONLY = 1 };
 enum { ARCHES_POLICY_ORACLE = 0, ARCHES_POLICY_FIXED = 1, ARCHES_POLICY_TREE = 2 };

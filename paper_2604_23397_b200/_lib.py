@@ -18,6 +18,7 @@ MAX_ANT, MAX_DMRS, MAX_SYM, MAX_BINS, MAX_MCS, MAX_TREE_NODES = 64, 4, 14, 64, 3
 EXEC_CONCURRENT, EXEC_SELECTED_ONLY = 0, 1
 POLICY_ORACLE, POLICY_FIXED, POLICY_TREE = 0, 1, 2
 FLAG_NO_TC_K1, FLAG_NO_TC_K2 = 0x1, 0x2
+FLAG_TX_PACKED = 0x4   # tx arguments are the packed QPSK wire format (include/arches.h)
 EXPERT_OUT_C128 = 0x100
 LLR_STRIDE = 6
 TRIGGERS = {0: "policy", 1: "failsafe", 2: "oracle", 3: "fixed"}

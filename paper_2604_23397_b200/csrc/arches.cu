@@ -239,7 +239,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
   if (p.window_length < 1 || p.dapp_window_slots < 1 || p.decision_period_slots < 1)
     return set_err(ARCHES_E_CONFIG, "window lengths and periods must be positive");
   if (p.assumed_delay_spread < 0) return set_err(ARCHES_E_CONFIG, "delay_spread must be >= 0");
-  if (p.flags & ~(ARCHES_FLAG_NO_TC_K1 | ARCHES_FLAG_NO_TC_K2))
+  if (p.flags & ~(ARCHES_FLAG_NO_TC_K1 | ARCHES_FLAG_NO_TC_K2 | ARCHES_FLAG_TX_PACKED))
     return set_err(ARCHES_E_CONFIG, "unknown flags 0x%x", (unsigned)p.flags);
   {
     // The device keeps in-flight control messages in fixed queues of
@@ -525,9 +525,12 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
       const int n_b = (ncol / 2) * 4 * d.tc_kb;  // B entries: <= 2 per thread of 512
       const int as = grp ? 4 : d.A;               // antennas per stage
       const int nbuf = 3;  // B operands in flight (k2_tc NBUF = LEAD + 1)
-      // two y (+ tx) stages; antenna groups keep the tile's tx rows in one extra buffer
-      sm = (2 * (size_t)(as + (grp ? 0 : 1)) + (grp ? 1 : 0)) * d.T * ARCHES_TILE * sizeof(float2) +
-           2 * nbuf * (size_t)d.tc_kb * ng * 256;
+      // two y (+ tx) stages; antenna groups keep the tile's tx rows in one extra buffer;
+      // packed tx: the tile's 2-bit codes (padded to 512 B) instead of its tx rows
+      sm = (p.flags & ARCHES_FLAG_TX_PACKED)
+               ? 2 * ((size_t)as * d.T * ARCHES_TILE * sizeof(float2) + 512)
+               : (2 * (size_t)(as + (grp ? 0 : 1)) + (grp ? 1 : 0)) * d.T * ARCHES_TILE * sizeof(float2);
+      sm += 2 * nbuf * (size_t)d.tc_kb * ng * 256;
       if (grp) sm += (size_t)21 * TC_THREADS * sizeof(float);  // MRC sums across groups
       if (sm > 227 * 1024 || n_b > 2 * TC_THREADS || ncol > 64) sm = 0;
       // the per-tile phase rotations in shared memory when they fit
@@ -540,6 +543,15 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
     }
     P->k2_tc_smem = sm;
     P->k2_groups = grp && sm ? d.A / 4 : 1;
+    d.tx_packed = (p.flags & ARCHES_FLAG_TX_PACKED) ? 1 : 0;
+    if (d.tx_packed && !(sm && !grp && std_pat && na == d.A && d.T * ARCHES_TXB_ROW <= 512)) {
+      cudaFree(buf);
+      if (P->k1t_wimg) cudaFree(P->k1t_wimg);
+      delete P;
+      return set_err(ARCHES_E_CONFIG,
+                     "ARCHES_FLAG_TX_PACKED needs the tensor-core K2 over one antenna group "
+                     "(n_ant 1, 2 or 4, DMRS symbols 0/5/10)");
+    }
   }
   if (P->k2_smem > 200 * 1024 && !(P->k2_tc_smem && P->k2_groups > 1)) {
     cudaFree(buf);
@@ -860,7 +872,31 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
   memset(&tm_x, 0, sizeof(tm_x));
   // tensor maps need 16-byte aligned bases; otherwise the CUDA-core loads
   const bool tmap = make_row_tmap(&tm_y, a.y, d.N, d.A * d.T, n_units, ngrp > 1 ? 4 * d.T : 0) &&
-                    make_row_tmap(&tm_x, a.tx, d.N, d.T, n_units);
+                    (d.tx_packed || make_row_tmap(&tm_x, a.tx, d.N, d.T, n_units));
+  if (d.tx_packed) {  // packed tx: y through the tensor map, the tile's codes by one bulk copy
+    if (!tmap || (reinterpret_cast<uintptr_t>(a.tx) & 15))
+      return set_err(ARCHES_E_CONTRACT, "packed tx needs 16-byte aligned y and tx");
+#define K2TC_PK(NA_)                                                                        \
+    if (d.A == NA_) {                                                                       \
+      auto kern = k2_tc<NA_, 3, true, true, false, true>;                                   \
+      CUDA_TRY(ensure_smem(kern, smem));                                                    \
+      CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(TC_BLOCK), smem, s, d, a, n_items, tm_y, tm_x)); \
+      LAUNCH_CHECK();                                                                       \
+    }
+    K2TC_PK(4) else K2TC_PK(2) else K2TC_PK(1) else return set_err(ARCHES_E_CONFIG, "packed tx: n_ant");
+#undef K2TC_PK
+    cudaStream_t s3 = s;
+    if (g_hook.k3_stream) {
+      CUDA_TRY(cudaEventRecord(g_hook.k2_done, s));
+      CUDA_TRY(cudaStreamWaitEvent(g_hook.k3_stream, g_hook.k2_done, 0));
+      s3 = g_hook.k3_stream;
+      g_hook.k3_on_tail = true;
+    }
+    k3_finalize<<<(n_units * 32 + K3_THREADS - 1) / K3_THREADS, K3_THREADS, 0, s3>>>(d, a, n_units,
+                                                                                     n_items, grid);
+    LAUNCH_CHECK();
+    return ARCHES_OK;
+  }
 #define K2TC_LAUNCH_G(NA_, ND_, STD_, GRP_)                                                  \
   {                                                                                          \
     auto kern = tmap ? k2_tc<NA_, ND_, STD_, true, GRP_> : k2_tc<NA_, ND_, STD_, false, GRP_>; \

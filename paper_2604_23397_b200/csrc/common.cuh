@@ -38,6 +38,7 @@ struct PlanDev {
   const float2* tc_rot;         // [n_tiles][4*tc_kb + 8]: e^{-2 pi i l k0/N} (AI), e^{-2 pi i l (k0-b*block)/N} (MMSE)
   int num_sms;
   int k2_rot_smem;              // tensor-core K2 stages tc_rot in shared memory
+  int tx_packed;                // ARCHES_FLAG_TX_PACKED: tx is the packed QPSK wire format
   // KPM layer
   double sinr_cap_db, lcid4_fraction, lcid4_jitter, crc_margin_db, crc_scale_db;
   double slot_us, slot_s;
@@ -195,4 +196,19 @@ __host__ __device__ inline bool k2_segment_start(int item, int n_tiles, int n_it
   }
   const long long b = ((long long)item * G + n_items - 1) / n_items;  // ceil
   return b < G && (b * n_items) / G == item;
+}
+
+// ---------------------------------------------------------------- packed tx
+// a 2-bit code of the QPSK wire format (bit 0: Re > 0, bit 1: Im > 0) as the
+// complex64 of qpsk() (rng.py:50-55); k_pack_qpsk / k_unpack_qpsk define it
+__device__ __forceinline__ float2 qpsk_code_to_x(unsigned int c) {
+  const float q = __uint_as_float(ARCHES_QPSK_AMP);
+  return make_float2((c & 1u) ? q : -q, (c & 2u) ? q : -q);
+}
+// RE (u, t, k) of a packed tx grid [u][n_tiles][T][32 B]
+__device__ __forceinline__ float2 tx_packed_at(const PlanDev& P, const unsigned char* bits, size_t u,
+                                               int t, int k) {
+  const int tile = k / ARCHES_TILE, j = k - tile * ARCHES_TILE;
+  const unsigned int b = bits[((u * P.n_tiles + tile) * P.T + t) * ARCHES_TXB_ROW + (j >> 2)];
+  return qpsk_code_to_x(b >> ((j & 3) * 2));
 }

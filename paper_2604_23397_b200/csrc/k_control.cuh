@@ -259,7 +259,7 @@ __global__ void k_tree_predict(const arches_tree* tree, const double* x, int n, 
   if (i < n) labels[i] = tree_descend(tree, x + (size_t)i * nf);
 }
 
-// tx[u][T][N] complex64 -> packed QPSK codes [u][n_tiles][T][32] (ARCHES_FLAG_TX_QPSK2);
+// tx[u][T][N] complex64 -> packed QPSK codes [u][n_tiles][T][32] (ARCHES_FLAG_TX_PACKED);
 // one thread per code byte (4 REs); any RE that is not exactly a qpsk() symbol
 // raises *bad
 __global__ void k_pack_qpsk(const PlanDev P, const float2* tx, unsigned char* bits, int32_t* bad,

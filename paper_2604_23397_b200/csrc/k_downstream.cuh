@@ -157,7 +157,9 @@ __global__ void __launch_bounds__(K6_THREADS) k_perturb_mmse(const PlanDev P, co
       float den;
       const float2 xh = xhat_re(P, h, yu, k, t, nv, den);
       if (even && P.is_dmrs[t] >= 0) continue;  // pilot RE
-      const float2 x = a.tx[((size_t)u * P.T + t) * P.N + k];
+      const float2 x = P.tx_packed
+                           ? tx_packed_at(P, reinterpret_cast<const unsigned char*>(a.tx), u, t, k)
+                           : a.tx[((size_t)u * P.T + t) * P.N + k];
       const double xr = x.x, xi = x.y, hr = xh.x, hi = xh.y;
       v[4] += xr * xr + xi * xi;
       v[6] += xr * hr + xi * hi;

@@ -230,10 +230,13 @@ __device__ __forceinline__ void eq_re_den(const float2 (&h)[NA][ND], const float
 // come from the DMRS Gram entries G_dd = sum_a |h_ad|^2 and R = sum_a Re(h_ad^*
 // h_a,d+1) of the half's DMRS pair: a held symbol's is G_dd (the same fma chain
 // as the direct sum), an interpolated one's w0^2 G00 + w1^2 G11 + 2 w0 w1 R.
-template <int NA, int ND, int H, bool SXX>
+// PK: tx from the packed QPSK wire format (xb = this subcarrier's code byte of
+// symbol 0, codes of later symbols ARCHES_TXB_ROW apart, jsh = its bit offset)
+template <int NA, int ND, int H, bool SXX, bool PK = false>
 __device__ __forceinline__ void eq_std_half(const float2 (&h)[NA][ND], const float2* yrow,
-                                            const float2* xrow, float modd, float nv, float& sre,
-                                            float& sim, float& syy, float& sxx) {
+                                            const float2* xrow, const unsigned char* xb, int jsh,
+                                            float modd, float nv, float& sre, float& sim,
+                                            float& syy, float& sxx) {
   // balanced halves: 4 interpolated + 3 held symbols each
   constexpr int kSym[2][7] = {{0, 1, 2, 3, 4, 5, 10}, {6, 7, 8, 9, 11, 12, 13}};
   static_assert(ND == 3, "NR 0/5/10 pattern");
@@ -260,7 +263,9 @@ __device__ __forceinline__ void eq_std_half(const float2 (&h)[NA][ND], const flo
     float2 yv[NA];
 #pragma unroll
     for (int a = 0; a < NA; ++a) yv[a] = yrow[(size_t)(a * 14 + t) * ARCHES_TILE];
-    const float2 x = xrow[(size_t)t * ARCHES_TILE];
+    float2 x;
+    if constexpr (PK) x = qpsk_code_to_x((unsigned int)xb[t * ARCHES_TXB_ROW] >> jsh);
+    else x = xrow[(size_t)t * ARCHES_TILE];
     const bool dm = (t == 0 || t == 5 || t == 10);
     const float m = dm ? modd : 1.f;
     float den;
@@ -345,7 +350,7 @@ __device__ __forceinline__ void eq_grp_half(const float2 (&h)[NA][ND], const flo
   }
 }
 
-template <int NA, int ND, bool kStd, bool kTmap, bool kGrp = false>
+template <int NA, int ND, bool kStd, bool kTmap, bool kGrp = false, bool kPk = false>
 __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
     k2_tc(const PlanDev P, const K2Args args, const int n_items,
           const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ CUtensorMap tm_x) {
@@ -392,7 +397,10 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
   // MIMO) the tile's tx rows live in ONE buffer next to the stages: only a tile's
   // last group reads them, and the load of the next tile's tx is issued after
   // that item's equaliser finished (the stage refill rule below)
-  const size_t stage_elems = (size_t)(AS + (kGrp ? 0 : 1)) * T * ARCHES_TILE;
+  static_assert(!kPk || (kStd && kTmap && !kGrp), "packed tx: single-group NR-pattern plans");
+  // packed tx (kPk): the tile's 2-bit codes (T x 32 B) after the y rows, padded to 512 B
+  const size_t stage_elems = kPk ? (size_t)AS * T * ARCHES_TILE + 64
+                                 : (size_t)(AS + (kGrp ? 0 : 1)) * T * ARCHES_TILE;
   const size_t coef_stride = coef_floats2(P);
   float2* sYX = reinterpret_cast<float2*>(sm);                               // [2][stage]
   float2* sX = sYX + 2 * stage_elems;                                         // [T][TILE] (kGrp)
@@ -456,10 +464,14 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
     if constexpr (kTmap) {  // lane 0: two tensor copies (y rows of the group, tx rows)
       if (lane == 0) {
         const size_t ybytes = (size_t)AS * T * ARCHES_TILE * sizeof(float2);
-        const size_t xbytes = (size_t)T * ARCHES_TILE * sizeof(float2);
+        const size_t xbytes = kPk ? (size_t)T * ARCHES_TXB_ROW : (size_t)T * ARCHES_TILE * sizeof(float2);
         mbar_arrive_expect_tx(&s_full[stage], (uint32_t)(with_x ? ybytes + xbytes : ybytes));
         tma_load_3d(dst, &tm_y, tile * 2 * ARCHES_TILE, gr * AS * T, u, &s_full[stage], pol);
-        if (with_x) tma_load_3d(xdst, &tm_x, tile * 2 * ARCHES_TILE, 0, u, &s_full[stage], pol);
+        if constexpr (kPk)
+          bulk_g2s(xdst, reinterpret_cast<const unsigned char*>(args.tx) + ((size_t)u * n_tiles + tile) * xbytes,
+                   (uint32_t)xbytes, &s_full[stage], pol);
+        else if (with_x)
+          tma_load_3d(xdst, &tm_x, tile * 2 * ARCHES_TILE, 0, u, &s_full[stage], pol);
       }
     } else {  // one 1-D bulk copy per row, rows spread over the lanes
       const int k0 = tile * ARCHES_TILE;
@@ -710,8 +722,10 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
         if (half == 0) eq_grp_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
         else           eq_grp_half<NA, ND, 1, true>(h, yrow, xrow, modd, nv, gacc, first, last, sre, sim, syy, sxx);
       } else if constexpr (kStd) {  // compile-time symbol half and expert: weights and pilot symbols fold
-        if (half == 0) eq_std_half<NA, ND, 0, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
-        else           eq_std_half<NA, ND, 1, true>(h, yrow, xrow, modd, nv, sre, sim, syy, sxx);
+        const unsigned char* xb = reinterpret_cast<const unsigned char*>(xrow - j) + (j >> 2);
+        const int jsh = (j & 3) * 2;
+        if (half == 0) eq_std_half<NA, ND, 0, true, kPk>(h, yrow, xrow, xb, jsh, modd, nv, sre, sim, syy, sxx);
+        else           eq_std_half<NA, ND, 1, true, kPk>(h, yrow, xrow, xb, jsh, modd, nv, sre, sim, syy, sxx);
       } else {
         const int t0 = half ? TH : 0, t1 = half ? T : TH;
         for (int t = t0; t < t1; ++t) {

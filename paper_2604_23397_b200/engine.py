@@ -89,7 +89,9 @@ class ArchesPlan:
         p.decision_delay_ns = latency.decision_delay_ns()
         p.failsafe_timeout_ns = dapp.timeout_ns(geometry.slot_duration_ns)
         p.crc_purpose_key = purpose_key("crc")
-        p.flags = int(flags)   # _lib.FLAG_NO_TC_K1 / FLAG_NO_TC_K2: force the CUDA-core kernels
+        p.flags = int(flags)   # _lib.FLAG_NO_TC_K1 / FLAG_NO_TC_K2: force the CUDA-core kernels;
+        # _lib.FLAG_TX_PACKED: the engine keeps tx in the packed QPSK wire format
+        self.flags = int(flags)
         self._geom, self._params = g, p
         h = C.c_void_p()
         _lib.check(_lib.lib().arches_plan_create(C.byref(g), C.byref(p), C.byref(h)))
@@ -143,7 +145,11 @@ class SlotEngine:
         self.device = dev
         U = self.U
         self.y = torch.zeros((U, A, T, N), dtype=torch.complex64, device=dev)
-        self.tx = torch.zeros((U, T, N), dtype=torch.complex64, device=dev)
+        # tx: the complex64 grid, or (plans with FLAG_TX_PACKED) the packed QPSK
+        # wire format K2 reads directly (2 bits per RE)
+        self.tx_packed = bool(plan.flags & _lib.FLAG_TX_PACKED)
+        self.tx = (torch.zeros((U, -(-N // 128), T, 32), dtype=torch.uint8, device=dev) if self.tx_packed
+                   else torch.zeros((U, T, N), dtype=torch.complex64, device=dev))
         self.pilots = torch.zeros((n_streams, self.M, D), dtype=torch.complex64, device=dev)
         self.noise_var = torch.zeros(U, dtype=torch.float64, device=dev)
         self.regime = torch.ones(U, dtype=torch.int8, device=dev)
@@ -213,9 +219,14 @@ class SlotEngine:
             dst.copy_(t, non_blocking=non_blocking)
 
         put(self.y, y, np.complex64)
-        if tx is not None and (tx.dtype == torch.uint8 if isinstance(tx, torch.Tensor)
-                               else np.asarray(tx).dtype == np.uint8):
+        packed_in = tx is not None and (tx.dtype == torch.uint8 if isinstance(tx, torch.Tensor)
+                                        else np.asarray(tx).dtype == np.uint8)
+        if packed_in:
             self._load_tx_bits(tx, non_blocking)
+        elif tx is not None and self.tx_packed:
+            grid = torch.empty((self.U, self.T, self.N), dtype=torch.complex64, device=self.device)
+            put(grid, tx, np.complex64)
+            self._pack_into(grid, self.tx)
         else:
             put(self.tx, tx, np.complex64)
         put(self.noise_var, noise_var, np.float64)
@@ -227,23 +238,32 @@ class SlotEngine:
         t = bits if isinstance(bits, torch.Tensor) else torch.from_numpy(np.asarray(bits))
         if tuple(t.shape) != shape:
             raise ContractViolation(f"packed tx shape {tuple(t.shape)}, expected {shape}")
+        if self.tx_packed:   # K2 reads the codes as they are
+            self.tx.copy_(t, non_blocking=non_blocking)
+            return
         if getattr(self, "_tx_bits", None) is None:
             self._tx_bits = torch.empty(shape, dtype=torch.uint8, device=self.device)
         self._tx_bits.copy_(t, non_blocking=non_blocking)
         _lib.check(_lib.lib().arches_unpack_qpsk(self.plan.handle, self.U, _lib.ptr(self._tx_bits),
                                                  _lib.ptr(self.tx), _stream_handle()))
 
+    def _pack_into(self, grid, out):
+        import torch
+        bad = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _lib.check(_lib.lib().arches_pack_qpsk(self.plan.handle, self.U, _lib.ptr(grid),
+                                               _lib.ptr(out), _lib.ptr(bad), _stream_handle()))
+        if int(bad.item()):
+            raise ContractViolation("tx grid is not QPSK (+-1 +-1j)/sqrt(2) in complex64")
+
     def pack_tx(self) -> np.ndarray:
         """The loaded transmit grids in the packed QPSK wire format (device packer;
         ContractViolation if any RE is not a qpsk() symbol)."""
         import torch
+        if self.tx_packed:
+            return self.tx.cpu().numpy()
         out = torch.empty((self.U, -(-self.N // 128), self.T, 32), dtype=torch.uint8,
                           device=self.device)
-        bad = torch.zeros(1, dtype=torch.int32, device=self.device)
-        _lib.check(_lib.lib().arches_pack_qpsk(self.plan.handle, self.U, _lib.ptr(self.tx),
-                                               _lib.ptr(out), _lib.ptr(bad), _stream_handle()))
-        if int(bad.item()):
-            raise ContractViolation("tx grid is not QPSK (+-1 +-1j)/sqrt(2) in complex64")
+        self._pack_into(self.tx, out)
         return out.cpu().numpy()
 
     # ------------------------------------------------------------ run

@@ -84,9 +84,13 @@ class DeviceScene:
         eng._settle()
         eng.regime.copy_(torch.from_numpy(r.reshape(-1)))
         zd = torch.from_numpy(z.reshape(-1)).to(eng.device)
+        tx = (torch.empty((eng.U, eng.T, eng.N), dtype=torch.complex64, device=eng.device)
+              if eng.tx_packed else eng.tx)
         _lib.check(_lib.lib().arches_synthesize(
             eng.plan.handle, eng.C, eng.S, _lib.ptr(self._seeds), self._regs, _lib.ptr(self._mask),
             self._sqrt_p, self._excess, _lib.ptr(eng.regime), _lib.ptr(zd), _lib.ptr(self.pilots),
-            _lib.ptr(self.state), _lib.ptr(self.ws), _lib.ptr(eng.y), _lib.ptr(eng.tx),
+            _lib.ptr(self.state), _lib.ptr(self.ws), _lib.ptr(eng.y), _lib.ptr(tx),
             _lib.ptr(eng.noise_var), torch.cuda.current_stream().cuda_stream))
+        if eng.tx_packed:   # synthesis writes the complex grid; the engine keeps its codes
+            eng._pack_into(tx, eng.tx)
         self.slot += eng.S
