@@ -63,9 +63,9 @@ struct arches_plan {
   int k1_parts;        // K1 CTAs per unit (comb analysis)
   size_t k1_smem;
   int k1t_nb;          // tensor-core K1: MMA N (0 = not applicable)
-  int k1t_nchunks;     // 16-subcarrier chunks per row
+  int k1t_nchunks;     // 256-subcarrier chunks per row
   float* k1t_wimg;     // twiddle operand [hi|lo][kg][nb][4] (chunk-invariant)
-  float2* k1t_rot;     // chunk phases [chunk][L]
+  float2* k1t_rot;     // sub-chunk phases [chunk * 8][K1T_LP]
   int k1_full_chunk;   // N-point (denoiser compat) variant
   int k1_full_parts;
   size_t k1_full_smem;
@@ -122,12 +122,19 @@ struct WsLayout {
   size_t coef, parts, counters, k1parts, k1counters, sigma2, rng, k1t_d, k1t_e, k1t_share, total;
 };
 
-// tensor-core K1 work split: 128-row tiles x DMRS symbols x subcarrier parts,
-// parts chosen so the items fill (at most) one wave of SMs
+// tensor-core K1 work split: (16-row tile, DMRS symbol, 256-subcarrier chunk)
+// items cut into one contiguous range per CTA (at most one wave of SMs); a
+// tile never straddles streams (gps tiles per stream)
 struct K1TGeom {
-  int n_g, parts, cpp, n_items;
+  int gps, n_g, n_items, grid;
 };
-static K1TGeom k1t_geom(const arches_plan* P, int n_units);
+static K1TGeom k1t_geom(const arches_plan* P, int n_streams, int n_slots);
+// workspace bound over every (streams, slots) split of n_units:
+// streams * ceil(slots * A / 16) <= units * ceil(A / 16)
+static int k1t_max_items(const arches_plan* P, int n_units) {
+  const PlanDev& d = P->dev;
+  return n_units * ((d.A + K1T_RR - 1) / K1T_RR) * d.D * P->k1t_nchunks;
+}
 
 // row chunks of the tensor-core K1 finalize: 1 (one CTA per unit, bins staged in
 // shared memory) unless a unit's bins exceed that stage
@@ -159,11 +166,11 @@ static WsLayout ws_layout(const arches_plan* P, int n_units) {
   off += align256((size_t)n_units * 2 * sizeof(double));
   w.k1t_d = w.k1t_e = w.k1t_share = off;
   if (P->k1t_nb) {
-    const K1TGeom kg = k1t_geom(P, n_units);
+    const size_t items = (size_t)k1t_max_items(P, n_units);
     w.k1t_d = off;
-    off += align256((size_t)kg.n_items * 128 * 2 * d.L * sizeof(double));
+    off += align256(items * K1T_RR * 2 * d.L * sizeof(double));
     w.k1t_e = off;
-    off += align256((size_t)kg.n_items * 128 * sizeof(double));
+    off += align256(items * K1T_RR * sizeof(double));
     w.k1t_share = off;  // row-chunked finalize: per-CTA energy / guard shares
     off += align256((size_t)n_units * k1t_fin_chunks(d) * 2 * sizeof(double));
   }
@@ -454,7 +461,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
     P->k1t_wimg = nullptr;
     P->k1t_nchunks = (N + K1T_CSC - 1) / K1T_CSC;
     const int nb = ((2 * d.L + 15) / 16) * 16;
-    if (d.diag && d.D <= 4 && d.L == 20 && P->k1t_nchunks <= K1T_MAX_CHUNKS &&
+    if (d.diag && d.D <= 4 && d.L == 20 && P->k1t_nchunks * K1T_SUBS <= K1T_MAX_SUB &&
         !(p.flags & ARCHES_FLAG_NO_TC_K1)) {  // k1_tc<48, 40>
       // chunk-invariant operand W[p][l] = e^{2 pi i l p / M} (p < 16 comb points),
       // real-embedded: kappa = 2p + (0: Re h, 1: Im h), row n = 2l + (0: Re, 1: Im);
@@ -484,13 +491,13 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
             img[half + o] = lo;
           }
         }
-      // chunk phases e^{2 pi i l 16c / M}
-      std::vector<float2> rot((size_t)P->k1t_nchunks * d.L);
-      for (int c = 0; c < P->k1t_nchunks; ++c)
+      // sub-chunk phases e^{2 pi i l 16c / M}, rows padded to K1T_LP
+      std::vector<float2> rot((size_t)P->k1t_nchunks * K1T_SUBS * K1T_LP, make_float2(0.f, 0.f));
+      for (int c = 0; c < P->k1t_nchunks * K1T_SUBS; ++c)
         for (int l = 0; l < d.L; ++l) {
           const long long idx = ((long long)l * K1T_CP * c) % M;
           const double ang = 2.0 * M_PI * (double)idx / (double)M;
-          rot[(size_t)c * d.L + l] = make_float2((float)cos(ang), (float)sin(ang));
+          rot[(size_t)c * K1T_LP + l] = make_float2((float)cos(ang), (float)sin(ang));
         }
       const size_t rot_off = (img.size() * sizeof(float) + 255) & ~(size_t)255;
       unsigned char* dimg = nullptr;
@@ -627,16 +634,13 @@ static int launch_k1(const arches_plan* P, int n_units, const Src& src, const K1
   return ARCHES_OK;
 }
 
-static K1TGeom k1t_geom(const arches_plan* P, int n_units) {
+static K1TGeom k1t_geom(const arches_plan* P, int n_streams, int n_slots) {
   const PlanDev& d = P->dev;
   K1TGeom g;
-  g.n_g = (n_units * d.A + 127) / 128;
-  const int base = g.n_g * d.D;
-  int parts = std::max(1, d.num_sms / std::max(1, base));
-  parts = std::min(parts, P->k1t_nchunks);
-  g.cpp = (P->k1t_nchunks + parts - 1) / parts;
-  g.parts = (P->k1t_nchunks + g.cpp - 1) / g.cpp;
-  g.n_items = base * g.parts;
+  g.gps = (n_slots * d.A + K1T_RR - 1) / K1T_RR;
+  g.n_g = n_streams * g.gps;
+  g.n_items = g.n_g * d.D * P->k1t_nchunks;
+  g.grid = std::max(1, std::min(g.n_items, d.num_sms));
   return g;
 }
 
@@ -647,49 +651,55 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncodeTiledFn encode_tiled();
 
-// DMRS symbol d of every (unit, antenna) row as a 2-D fp32 view {2N floats,
-// rows}; box {32 floats, 128 rows} lands 128 rows x 16 subcarriers in the
-// UMMA K-major SWIZZLE_128B layout
-static bool make_k1t_tmap(CUtensorMap* m, const float2* y, const PlanDev& d, int dsym, int rows) {
-  EncodeTiledFn enc = encode_tiled();
-  const float2* base = y + (size_t)dsym * d.N;
-  if (!enc || (d.N & 1) || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)2 * d.N, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)8 * d.T * d.N};
-  const cuuint32_t box[2] = {32, 128};  // 128 B (the swizzle span) x 128 rows
-  const cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+// launch with programmatic stream serialization: the kernel may start while the
+// previous kernel of the stream drains and synchronises with griddepcontrol.wait
+template <typename K, typename... Args>
+static cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 static int launch_k1t(const arches_plan* P, int n_units, const GridCombSrc& src, const K1Out& o,
                       const WsLayout& w, void* ws, cudaStream_t s) {
   const PlanDev& d = P->dev;
-  const K1TGeom kg = k1t_geom(P, n_units);
+  const K1TGeom kg = k1t_geom(P, n_units / src.n_slots, src.n_slots);
+  if ((long long)kg.n_items * kg.grid >= (1LL << 31)) return set_err(ARCHES_E_CONFIG, "K1: batch too large");
   K1TArgs a;
+  a.y = src.y;
   a.pil = src.pil;
   a.wimg = P->k1t_wimg;
   a.rot = P->k1t_rot;
   a.dpart = ws_at<double>(ws, w.k1t_d);
   a.epart = ws_at<double>(ws, w.k1t_e);
   a.n_slots = src.n_slots;
+  a.srows = src.n_slots * d.A;
   a.n_rows = n_units * d.A;
+  a.gps = kg.gps;
   a.n_g = kg.n_g;
-  a.parts = kg.parts;
-  a.cpp = kg.cpp;
   a.n_chunks = P->k1t_nchunks;
+  a.n_items = kg.n_items;
+  a.grid = kg.grid;
   a.nb = P->k1t_nb;
-  CUtensorMap tm[4];
-  memset(tm, 0, sizeof(tm));
-  for (int dd = 0; dd < d.D; ++dd)
-    if (!make_k1t_tmap(&tm[dd], src.y, d, d.dsym[dd], a.n_rows))
-      return set_err(ARCHES_E_CUDA, "K1: tensor map encode failed");
-  const int grid = std::min(kg.n_items, d.num_sms);
-  const size_t smem = k1t_smem_bytes(a.nb);
+  if ((reinterpret_cast<uintptr_t>(src.y) & 15) || (d.N & 1))
+    return set_err(ARCHES_E_CONTRACT, "K1: grid rows must be 16-byte aligned");
+  const int grid = kg.grid;
+  const size_t smem = k1t_smem_bytes(a.nb, a.n_chunks);
   const int nchunk = k1t_fin_chunks(d);
   CUDA_TRY(ensure_smem(k1_tc<48, 40>, smem));
-  k1_tc<48, 40><<<grid, K1T_THREADS, smem, s>>>(d, a, kg.n_items, tm[0], tm[1], tm[2], tm[3]);
+  // (a programmatic launch behind the previous batch's K2 measured 2.4% slower
+  // per step: its waiting CTAs take SMs from the tail stream's K3 / K4)
+  k1_tc<48, 40><<<grid, K1T_THREADS, smem, s>>>(d, a);
   LAUNCH_CHECK();
   if (g_hook.before_fin) CUDA_TRY(cudaStreamWaitEvent(s, g_hook.before_fin, 0));
   {
@@ -838,25 +848,6 @@ static bool make_row_tmap(CUtensorMap* m, const void* base, int N, int rows, int
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// launch with programmatic stream serialization: the kernel may start while the
-// previous kernel of the stream drains and synchronises with griddepcontrol.wait
-template <typename K, typename... Args>
-static cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              Args... args) {
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cudaStream_t s) {
@@ -1447,3 +1438,12 @@ extern "C" int32_t arches_device_available(void) {
   }
   return n > 0 ? 1 : 0;
 }
+
+#ifdef K1T_TRACE
+extern "C" int arches_k1t_trace(void* host) {
+  return cudaMemcpyFromSymbol(host, g_k1t_trace, sizeof(g_k1t_trace)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int arches_k1t_span(void* host) {
+  return cudaMemcpyFromSymbol(host, g_k1t_span, sizeof(g_k1t_span)) == cudaSuccess ? 0 : 1;
+}
+#endif

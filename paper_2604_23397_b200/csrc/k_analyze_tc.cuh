@@ -4,52 +4,82 @@
 // Replaces the analysis half of ls_estimate / estimate_noise_var /
 // mmse_estimate / denoiser_estimate (expert_bank.py:96-214):
 //   B[u,a,d][l] = sum_m h[u,a,d][m] e^{+2 pi i l m / M},  h = y[.., 2m, dmrs_d] conj(p) / |p|^2
-// written as  D[row][n] = sum_kappa A[row][kappa] W[kappa][n]  with
-//   row   = u*A + a (128 rows per tile = 128/A units),
-//   kappa = real embedding of the subcarriers (odd subcarriers meet zero
-//           twiddles, so the raw grid rows are the operand, no gather),
+// written as  D[t][n] = sum_kappa A[t][kappa] W[kappa][n]  per chunk, with
+//   t     = MMA row = (data row rr, sub-chunk c): 16 data rows (row = u*A + a, one
+//           stream per tile) x 8 sub-chunks of 16 comb points, so one chunk
+//           spans 256 contiguous subcarriers (2 KB) of each of 16 rows,
+//   kappa = real embedding of the sub-chunk's 16 comb points,
 //   n     = 2l + re/im (N = 2L padded to 16).
-// Work item = (row tile g, DMRS symbol d, subcarrier part q); a CTA walks its
-// items in chunks of 16 subcarriers (8 comb points starting at m0 = 8c):
-//   D_c[row][l] = e^{2 pi i l m0/M} sum_{k<8} h[m0+k] e^{2 pi i l k/M}
-// so the MMA operand W (k < 8, real-embedded, tf32 hi | lo) is the same for
-// every chunk and stays in shared memory; the chunk's phase is applied to the
-// 2L outputs in the epilogue.
-//   * producer warp: one 2-D tensor TMA per chunk lands the raw DMRS row
-//     segments of 128 rows (128 B each) in the UMMA K-major SWIZZLE_128B layout
-//     (16-byte group g of row r at r*128 + (g ^ (r & 7))*16) in an 8-deep ring;
-//   * converter warps (thread = row = TMEM lane): h = y conj(p)/|p|^2 on the
-//     comb subcarriers, zero on the odd ones, tf32 hi | lo split into one of two
-//     MMA operand buffers (the raw stage is released right away);
-//   * MMA warp: D_c = A_hi W_hi + A_lo W_hi + A_hi W_lo (kind::tf32, 3xTF32)
-//     into a ring of TMEM accumulators;
-//   * converter warps, two chunks behind: tcgen05.ld of the row's 2L columns,
-//     the chunk phase, fp32 sums over 4 chunks folded into fp64 (short fp32
-//     chains keep the Parseval noise estimate precise); at the item end the
-//     partial bins (fp64) and the row energy go to global memory.
+// Sub-chunk cc (comb points m0 = 16 cc .. m0 + 15) contributes
+//   e^{2 pi i l m0/M} sum_{k<16} h[m0+k] e^{2 pi i l k/M}
+// so the MMA operand W (k < 16, real-embedded, tf32 hi | lo) is the same for
+// every chunk and stays in shared memory; each MMA row's sub-chunk phase is
+// applied to its 2L outputs in the epilogue and the 8 sub-chunks of a data row
+// are summed across lanes when its segment ends.
+//   * producer warp: per chunk, 16 lanes each issue one 1-D bulk copy of a
+//     row's 2 KB into a 16-byte-padded row of the stage (long row requests --
+//     the old 128-B swizzled tensor boxes made K1 TMA-request bound -- and the
+//     padding makes the converters' natural-order reads bank-conflict free);
+//   * converter warps: the 128 pilot inverses conj(p)/|p|^2 of the chunk, one per
+//     thread, into shared memory; then thread tau converts MMA row (rr, c) with
+//     rr = (tau/8 + c) mod 16, c = tau mod 8 (a quarter warp reads 8 rows at 8
+//     bank offsets and writes 8 SWIZZLE_128B groups): h = y q, tf32 hi | lo into
+//     one of two MMA operand buffers (the raw stage is released right away);
+//   * MMA warp: D = A_hi W_hi + A_lo W_hi + A_hi W_lo (kind::tf32, 3xTF32) into a
+//     ring of TMEM accumulators;
+//   * drain warps (thread = TMEM lane = MMA row): tcgen05.ld of the row's 2L
+//     columns, the sub-chunk phase, fp32 sums over 4 chunks folded into fp64
+//     (short fp32 chains keep the Parseval noise estimate precise); at a
+//     segment end (row tile change or the CTA's last chunk) the 8 sub-chunk
+//     lanes of a data row are summed (fp64 xor shuffles) and the segment's
+//     partial bins / row energy go to global memory.
+// Work split: the (row tile, DMRS symbol, chunk) items in that order, cut into
+// one contiguous range per CTA (balanced to one chunk); the finalize sums a
+// row's segments in chunk order, a segment starting at chunk 0 or at a CTA's
+// first item (k1t_row_sum).
 #pragma once
 #include "k_analyze.cuh"
 #include "k_synth_tc.cuh"
 
-#define K1T_CONV_WARPS 4                         // converters: warps 0-3, drains: warps 4-7
-#define K1T_THREADS (32 * (2 * K1T_CONV_WARPS + 2))  // + producer + MMA warp
-#define K1T_MAX_CHUNKS 112                       // phase table in shared memory (N <= 3584)
+#define K1T_CONV_WARPS 4                         // converters: warps 0-3
+#define K1T_DRAIN_WARPS 8                        // drains: warps 4-11 (two column halves)
+#define K1T_THREADS (32 * (K1T_CONV_WARPS + K1T_DRAIN_WARPS + 2))  // + producer + MMA warp
+#define K1T_NB 48                                // MMA N (2L = 40 padded to 16)
+#define K1T_MAX_SUB 112                          // sub-chunk phases in shared memory (N <= 3584)
 #define K1T_STAGES 4                             // raw grid stages
 #define K1T_MBUF 2                               // MMA operand buffers
-#define K1T_CSC 32                               // subcarriers per chunk (2 x 128-B TMA boxes)
-#define K1T_CP (K1T_CSC / 2)                     // comb points per chunk (one 128-B operand row)
+#define K1T_RR 16                                // data rows per item
+#define K1T_SUBS 8                               // sub-chunks per item (MMA rows = K1T_RR x K1T_SUBS)
+#define K1T_CP 16                                // comb points per sub-chunk (one 128-B operand row)
+#define K1T_CSC (2 * K1T_CP * K1T_SUBS)          // subcarriers per chunk (256 = one 2-KB row copy)
 #define K1T_ACC 4                                // TMEM accumulator ring
+#define K1T_LP 21                                // phase-table row stride (float2): conflict-free per-lane rows
+#define K1T_QP 18                                // pilot-inverse row stride per sub-chunk (float2)
 
 struct K1TArgs {
+  const float2* y;         // [u][A][T][N] grid
   const float2* pil;       // [stream][M][D]
   const float* wimg;       // [hi | lo][NB rows][128 B, SWIZZLE_128B] twiddle operand, chunk-invariant
-  const float2* rot;       // [n_chunks][L] chunk phases e^{2 pi i l 8c / M}
-  double* dpart;           // [item][128][2L] partial bins (fp64)
-  double* epart;           // [item][128] row energies
-  int n_slots, n_rows;     // rows = units * A
-  int n_g, parts, cpp;     // row tiles, subcarrier parts, chunks per part
-  int n_chunks, nb;        // chunks per row, MMA N
+  const float2* rot;       // [n_chunks * 8][K1T_LP] sub-chunk phases e^{2 pi i l 16cc / M}
+  double* dpart;           // [item][16][2L] segment partial bins (fp64), written at segment starts
+  double* epart;           // [item][16] segment row energies
+  int n_slots, srows;      // slots per stream, rows per stream (= n_slots * A)
+  int n_rows;              // rows of the grid (= units * A)
+  int gps;                 // 16-row tiles per stream (a tile never straddles streams)
+  int n_g, n_chunks;       // 16-row tiles, 256-subcarrier chunks per row
+  int n_items, grid;       // items = n_g * D * n_chunks, cut into `grid` contiguous ranges
+  int nb;                  // MMA N
 };
+
+// CTA b's items are [k1t_first(b), k1t_first(b + 1)); 32-bit products
+// (n_items * grid < 2^31 is checked at launch)
+__host__ __device__ __forceinline__ int k1t_first(int b, int n_items, int grid) {
+  return (int)(((unsigned)b * (unsigned)n_items) / (unsigned)grid);
+}
+// the CTA whose range holds item i
+__device__ __forceinline__ int k1t_owner(int i, int n_items, int grid) {
+  return (int)(((unsigned)(i + 1) * (unsigned)grid - 1u) / (unsigned)n_items);
+}
 
 // RNG side products of each unit (Philox CRC uniform of rng.stream(seed, "crc",
 // slot), LCID4 split of _lcid4_jitter(slot); rng.py:24-34, phy_pipeline.py:
@@ -71,9 +101,40 @@ __global__ void k_rng_units(const PlanDev P, double* rng, const uint64_t* seeds,
   rng[2 * u + 1] = fmin(fmax(f, 0.0), 1.0);
 }
 
-constexpr uint32_t K1T_ATOM = 128 * 128;           // 128 rows x 128 B (one SWIZZLE_128B K block)
-constexpr uint32_t K1T_RAW_BYTES = 2 * K1T_ATOM;    // raw chunk: 32 subcarriers of 128 rows
-constexpr uint32_t K1T_OP_BYTES = K1T_ATOM;         // compacted operand: 16 comb points of 128 rows
+#ifdef K1T_TRACE  // timing-analysis builds only (tools/k1_trace.py), never the shipped library
+__device__ unsigned long long g_k1t_trace[8][64][8];
+__device__ unsigned long long g_k1t_span[256][5];  // per CTA: entry, first copy, drain done, zeroed, synced
+#define K1TS(slot, cond)                                         \
+  do {                                                           \
+    if ((cond) && blockIdx.x < 256) {                            \
+      unsigned long long t_;                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));     \
+      g_k1t_span[blockIdx.x][(slot)] = t_;                       \
+    }                                                            \
+  } while (0)
+#define K1TR(slot, jj, cond)                                                          \
+  do {                                                                                \
+    if ((cond) && blockIdx.x < 8 && (jj) < 64) {                                      \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_k1t_trace[blockIdx.x][(jj)][(slot)] = t_;                                     \
+    }                                                                                 \
+  } while (0)
+#else
+#define K1TR(slot, jj, cond) \
+  do {                       \
+  } while (0)
+#define K1TS(slot, cond) \
+  do {                   \
+  } while (0)
+#endif
+
+constexpr uint32_t K1T_ATOM = 128 * 128;                        // 128 MMA rows x 128 B (one SWIZZLE_128B K block)
+constexpr uint32_t K1T_ROWB = K1T_CSC * 8;                       // 2 KB: one row of a chunk (complex64)
+constexpr uint32_t K1T_ROWP = K1T_ROWB + 16;                     // padded row stride in the stage
+constexpr uint32_t K1T_RAW_BYTES = K1T_RR * K1T_ROWP;            // raw chunk: 16 rows x 256 subcarriers
+constexpr uint32_t K1T_OP_BYTES = K1T_ATOM;                      // compacted operand: 16 comb points of 128 rows
+static_assert(K1T_STAGES * K1T_RAW_BYTES % 1024 == 0, "operand buffers stay 1024-byte aligned");
 
 // K-major SWIZZLE_128B shared-memory descriptor (8-row atoms of 128 B, 1024-B aligned)
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -85,289 +146,377 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;            // SWIZZLE_128B
   return d;
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
+
+__host__ __device__ inline size_t k1t_smem_bytes(int nb, int n_chunks) {
+  return (size_t)K1T_STAGES * K1T_RAW_BYTES + (size_t)K1T_MBUF * 2 * K1T_OP_BYTES +
+         (size_t)nb * 128 * 2 + (size_t)n_chunks * K1T_SUBS * K1T_LP * sizeof(float2);
 }
 
-__host__ __device__ inline size_t k1t_smem_bytes(int nb) {
-  return (size_t)K1T_STAGES * K1T_RAW_BYTES + (size_t)K1T_MBUF * 2 * K1T_OP_BYTES +
-         (size_t)nb * 128 * 2 + (size_t)K1T_MAX_CHUNKS * 20 * sizeof(float2);
+// item = (row tile g, DMRS symbol d, chunk ch), chunk fastest; walked incrementally
+struct K1TItem {
+  int g, d, ch;
+  __device__ __forceinline__ void init(int item, int nc, int D) {
+    ch = item % nc;
+    const int gd = item / nc;
+    d = gd % D;
+    g = gd / D;
+  }
+  __device__ __forceinline__ void next(int nc, int D) {
+    if (++ch == nc) {
+      ch = 0;
+      if (++d == D) d = 0, ++g;
+    }
+  }
+};
+
+// Drain of columns [C0, C0 + NC) of every chunk's accumulator: thread = MMA
+// row t = TMEM lane = (rr, c).  Phase-rotated chunk sums are added in fp32 over
+// K1T_FGRP chunks, then folded into fp64 (every fp32 chain stays short, so the
+// Parseval noise estimate keeps its precision); at a segment end the 8
+// sub-chunk lanes of a data row are summed by xor shuffles and the segment's
+// partial bins go to global memory.
+template <int NC, int C0>
+__device__ __forceinline__ void k1t_drain(const K1TArgs& a, int L, int t, uint32_t lane_base,
+                                          const float2* rotsm, uint64_t* s_accf, uint64_t* s_acce,
+                                          int i_begin, int i_end, int nc, int D) {
+  constexpr int K1T_FGRP = 4;
+  constexpr int NW = NC / K1T_SUBS;  // columns each lane of a data row writes
+  static_assert(NC % 2 == 0 && NC % K1T_SUBS == 0, "column split");
+  const int rr = t >> 3, c = t & 7, ncol = 2 * L;
+  float acc[NC];
+  double acc64[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) acc[q] = 0.f, acc64[q] = 0.0;
+  int seg = i_begin, nf = 0;
+  K1TItem it;
+  it.init(i_begin, nc, D);
+  for (int item = i_begin, j = 0; item < i_end; ++item, ++j, it.next(nc, D)) {
+    const int r = j % K1T_ACC;
+    mbar_wait_spin(&s_accf[r], (j / K1T_ACC) & 1);
+    K1TR(5 + (C0 > 0), j, t == 0);
+    tc_fence_after();
+    float vals[NC];
+    tmem_ld_n<NC>(lane_base + (uint32_t)(r * K1T_NB + C0), vals);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    mbar_arrive(&s_acce[r]);
+    const float2* ph = rotsm + (size_t)(it.ch * K1T_SUBS + c) * K1T_LP + C0 / 2;
+#pragma unroll
+    for (int l = 0; l < NC / 2; ++l) {
+      const float2 v = cmul(make_float2(vals[2 * l], vals[2 * l + 1]), ph[l]);
+      acc[2 * l] += v.x;
+      acc[2 * l + 1] += v.y;
+    }
+    const bool seg_end = item + 1 == i_end || it.ch + 1 == nc;
+    if (++nf == K1T_FGRP || seg_end) {
+      nf = 0;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        acc64[q] += (double)acc[q];
+        acc[q] = 0.f;
+      }
+    }
+    K1TR(7, j, t == 0 && C0 == 0);
+    if (seg_end) {
+      // reduce-scatter over the row's 8 lanes: at xor distance 4, 2, 1 a lane
+      // keeps the half of its remaining columns whose owner shares its bit and
+      // sends the other half, ending with its own NW columns [NW c, NW c + NW)
+      // summed over the 8 sub-chunks (fixed order: deterministic)
+      double r4[NC / 2], r2[NC / 4], r1[NW];
+      {
+        const bool hi = c & 4;
+#pragma unroll
+        for (int q = 0; q < NC / 2; ++q) {
+          const double mine = hi ? acc64[NC / 2 + q] : acc64[q];
+          const double send = hi ? acc64[q] : acc64[NC / 2 + q];
+          r4[q] = mine + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+      }
+      {
+        const bool hi = c & 2;
+#pragma unroll
+        for (int q = 0; q < NC / 4; ++q) {
+          const double mine = hi ? r4[NC / 4 + q] : r4[q];
+          const double send = hi ? r4[q] : r4[NC / 4 + q];
+          r2[q] = mine + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+      }
+      {
+        const bool hi = c & 1;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+          const double mine = hi ? r2[NW + q] : r2[q];
+          const double send = hi ? r2[q] : r2[NW + q];
+          r1[q] = mine + __shfl_xor_sync(0xffffffffu, send, 1);
+        }
+      }
+      const int stream = it.g / a.gps, lrow = (it.g - stream * a.gps) * K1T_RR + rr;
+      if (lrow < a.srows) {
+        double* dst = a.dpart + ((size_t)seg * K1T_RR + rr) * ncol + C0 + NW * c;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) dst[q] = r1[q];
+      }
+#pragma unroll
+      for (int q = 0; q < NC; ++q) acc64[q] = 0.0;
+      seg = item + 1;
+    }
+  }
 }
 
 template <int NB, int LC>
-__global__ void __launch_bounds__(K1T_THREADS, 1)
-    k1_tc(const PlanDev P, const K1TArgs a, const int n_items,
-          const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
-          const __grid_constant__ CUtensorMap tm2, const __grid_constant__ CUtensorMap tm3) {
+__global__ void __launch_bounds__(K1T_THREADS, 1) k1_tc(const PlanDev P, const K1TArgs a) {
   extern __shared__ __align__(1024) unsigned char sm1k[];
   __shared__ __align__(8) uint64_t s_full[K1T_STAGES], s_empty[K1T_STAGES];
   __shared__ __align__(8) uint64_t s_conv[K1T_MBUF], s_mfree[K1T_MBUF], s_w;
   __shared__ __align__(8) uint64_t s_accf[K1T_ACC], s_acce[K1T_ACC];
+  __shared__ __align__(16) float2 s_q[2][K1T_SUBS * K1T_QP];  // pilot inverses of a chunk, per sub-chunk row
+  __shared__ double s_e[128];                                 // segment energies per MMA row
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int nb = NB;
   constexpr uint32_t w_bytes = (uint32_t)nb * 128;
   const int NT = 32 * K1T_CONV_WARPS;
-  const int G = gridDim.x;
-  const int cpp = a.cpp;
-  unsigned char* raw = sm1k;                                            // [STAGES][2 atoms]
+  const int nc = a.n_chunks, D = P.D;
+  const int i_begin = k1t_first(blockIdx.x, a.n_items, a.grid);
+  const int i_end = k1t_first(blockIdx.x + 1, a.n_items, a.grid);
+  unsigned char* raw = sm1k;                                            // [STAGES][16 padded rows]
   unsigned char* mbuf = sm1k + (size_t)K1T_STAGES * K1T_RAW_BYTES;      // [MBUF][hi | lo]
   unsigned char* wbuf = mbuf + (size_t)K1T_MBUF * 2 * K1T_OP_BYTES;   // [hi | lo]
-  float2* rotsm = reinterpret_cast<float2*>(wbuf + 2 * w_bytes);      // [n_chunks][L] chunk phases
+  float2* rotsm = reinterpret_cast<float2*>(wbuf + 2 * w_bytes);      // [sub-chunk][K1T_LP] phases
 
-  if (threadIdx.x == 0) {
-    if (smem_u32(sm1k) & 1023u) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
-    for (int s = 0; s < K1T_STAGES; ++s) {
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], NT);
-    }
-    for (int b = 0; b < K1T_MBUF; ++b) {
-      mbar_init(&s_conv[b], NT);
-      mbar_init(&s_mfree[b], 1);
-    }
-    mbar_init(&s_w, 1);
-    for (int r = 0; r < K1T_ACC; ++r) {
-      mbar_init(&s_accf[r], 1);
-      mbar_init(&s_acce[r], NT);
-    }
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-        smem_u32(&s_tmem)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  K1TS(0, threadIdx.x == 0);
+  {
+    // barriers initialised one per thread (SWIZZLE_128B atoms need a 1024-byte-aligned base)
+    const int k = threadIdx.x;
+    if (k == 0 && (smem_u32(sm1k) & 1023u)) __trap();
+    if (k < K1T_STAGES) mbar_init(&s_full[k], 1);
+    else if (k < 2 * K1T_STAGES) mbar_init(&s_empty[k - K1T_STAGES], NT);
+    else if (k < 2 * K1T_STAGES + K1T_MBUF) mbar_init(&s_conv[k - 2 * K1T_STAGES], NT);
+    else if (k < 2 * K1T_STAGES + 2 * K1T_MBUF) mbar_init(&s_mfree[k - 2 * K1T_STAGES - K1T_MBUF], 1);
+    else if (k < 2 * K1T_STAGES + 2 * K1T_MBUF + K1T_ACC) mbar_init(&s_accf[k - 2 * K1T_STAGES - 2 * K1T_MBUF], 1);
+    else if (k < 2 * K1T_STAGES + 2 * K1T_MBUF + 2 * K1T_ACC)
+      mbar_init(&s_acce[k - 2 * K1T_STAGES - 2 * K1T_MBUF - K1T_ACC], 32 * K1T_DRAIN_WARPS);
+    else if (k == 2 * K1T_STAGES + 2 * K1T_MBUF + 2 * K1T_ACC) mbar_init(&s_w, 1);
   }
   // the finalize (programmatic dependent launch) may be scheduled onto SMs as
   // they free up; it waits for this grid's completion before reading anything
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = s_tmem;
+  __syncthreads();  // barriers initialised; the TMEM allocation is off this path (MMA warp)
+  constexpr int NTMEM = 32 + 32 * K1T_DRAIN_WARPS;  // MMA warp + drains: barriers 1 (alloc), 2 (release)
 
-  auto item_chunks = [&](int item, int& g, int& d, int& c0, int& c1) {
-    g = item % a.n_g;
-    const int r = item / a.n_g;
-    d = r % P.D;
-    const int q = r / P.D;
-    c0 = q * cpp;
-    c1 = min(c0 + cpp, a.n_chunks);
-  };
-
-  if (warp == 2 * K1T_CONV_WARPS) {
-    // ---------------- producer: the twiddle operand once, then raw chunks
+  static_assert(NB == K1T_NB, "MMA N");
+  if (warp == K1T_CONV_WARPS + K1T_DRAIN_WARPS) {
+    // ---------------- producer: the twiddle operand once, then raw chunks (lane = row)
+    const uint64_t pol_y = l2_evict_first_policy();
+    K1TS(3, lane == 0);
     if (lane == 0) {
-      const uint64_t pol_y = l2_evict_first_policy(), pol_w = l2_evict_last_policy();
-      const uint32_t rot_bytes = (uint32_t)(a.n_chunks * P.L * sizeof(float2) + 15) & ~15u;
+      const uint64_t pol_w = l2_evict_last_policy();
+      const uint32_t rot_bytes = (uint32_t)(nc * K1T_SUBS * K1T_LP * sizeof(float2) + 15) & ~15u;
       mbar_arrive_expect_tx(&s_w, 2 * w_bytes + rot_bytes);
       bulk_g2s(wbuf, a.wimg, 2 * w_bytes, &s_w, pol_w);
       bulk_g2s(rotsm, a.rot, rot_bytes, &s_w, pol_w);
-      int j = 0;
-      for (int item = blockIdx.x; item < n_items; item += G) {
-        int g, d, c0, c1;
-        item_chunks(item, g, d, c0, c1);
-        const CUtensorMap* tm = d == 0 ? &tm0 : d == 1 ? &tm1 : d == 2 ? &tm2 : &tm3;
-        for (int c = c0; c < c1; ++c, ++j) {
-          const int s = j % K1T_STAGES;
-          if (j >= K1T_STAGES) {
-            mbar_wait_spin(&s_empty[s], ((j / K1T_STAGES) - 1) & 1);
-          }
-          mbar_arrive_expect_tx(&s_full[s], K1T_RAW_BYTES);
-          unsigned char* dst = raw + (size_t)s * K1T_RAW_BYTES;
-          tma_load_2d(dst, tm, 2 * K1T_CSC * c, g * 128, &s_full[s], pol_y);
-          tma_load_2d(dst + K1T_ATOM, tm, 2 * K1T_CSC * c + 32, g * 128, &s_full[s], pol_y);
+    }
+    const size_t rowstride = (size_t)P.T * P.N;  // float2 between consecutive (unit, antenna) rows
+    K1TItem it;
+    it.init(i_begin, nc, D);
+    for (int item = i_begin, j = 0; item < i_end; ++item, ++j, it.next(nc, D)) {
+      const int s = j % K1T_STAGES;
+      const int stream = it.g / a.gps, lrow0 = (it.g - stream * a.gps) * K1T_RR;
+      const int nrows = min(K1T_RR, a.srows - lrow0);
+      // every copied row is a full 2 KB: a row's last chunk runs on into the next
+      // OFDM symbol's subcarriers (finite grid values, met by zero pilot
+      // inverses), except past the end of the grid (a DMRS symbol last in the
+      // slot, on the grid's last row), where the stage row's tail is zeroed
+      const uint32_t bytes = K1T_ROWB;
+      const int last = stream * a.srows + lrow0 + nrows;  // one past the tile's last row
+      const bool clamp = it.ch == nc - 1 && P.dsym[it.d] == P.T - 1 && last == a.n_rows;
+      const uint32_t tail = (uint32_t)(P.N - it.ch * K1T_CSC) * 8;
+      if (j >= K1T_STAGES) mbar_wait_spin(&s_empty[s], ((j / K1T_STAGES) - 1) & 1);
+      K1TR(0, j, lane == 0);
+      K1TS(1, lane == 0 && j == 0);
+      if (lane == 0) mbar_arrive_expect_tx(&s_full[s], (uint32_t)nrows * bytes - (clamp ? bytes - tail : 0u));
+      __syncwarp();
+      if (lane < nrows) {
+        const size_t grow = (size_t)(stream * a.srows + lrow0 + lane);
+        const float2* src = a.y + grow * rowstride + (size_t)P.dsym[it.d] * P.N + (size_t)it.ch * K1T_CSC;
+        unsigned char* dst = raw + (size_t)s * K1T_RAW_BYTES + lane * K1T_ROWP;
+        uint32_t nb_copy = bytes;
+        if (clamp && lane == nrows - 1) {
+          nb_copy = tail;
+          for (uint32_t o = tail; o < K1T_ROWB; o += 16)
+            *reinterpret_cast<float4*>(dst + o) = make_float4(0.f, 0.f, 0.f, 0.f);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
+        bulk_g2s(dst, src, nb_copy, &s_full[s], pol_y);
       }
     }
     return;
   }
-  if (warp == 2 * K1T_CONV_WARPS + 1) {
-    // ---------------- MMA issuer: chunk j -> TMEM accumulator j % K1T_ACC
+  if (warp == K1T_CONV_WARPS + K1T_DRAIN_WARPS + 1) {
+    // ---------------- MMA issuer: chunk j -> TMEM accumulator j % K1T_ACC; owns the TMEM
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    tc_fence_before();
+    named_bar(1, NTMEM);
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
     if (lane == 0) {
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(nb >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
       const uint32_t wh = smem_u32(wbuf), wl = wh + w_bytes;
       mbar_wait_spin(&s_w, 0);
-      int j = 0;
-      for (int item = blockIdx.x; item < n_items; item += G) {
-        int g, d, c0, c1;
-        item_chunks(item, g, d, c0, c1);
-        for (int c = c0; c < c1; ++c, ++j) {
-          const int b = j % K1T_MBUF, r = j % K1T_ACC;
-          {
-            if (j >= K1T_ACC) mbar_wait_spin(&s_acce[r], ((j / K1T_ACC) - 1) & 1);
-          }
-          {
-            mbar_wait_spin(&s_conv[b], (j / K1T_MBUF) & 1);
-          }
-          tc_fence_after();
-          const uint32_t dcol = tmem + (uint32_t)(r * nb);
-          const uint32_t ah = smem_u32(mbuf + (size_t)b * 2 * K1T_OP_BYTES), al = ah + K1T_OP_BYTES;
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {  // 8 tf32 (32 B) per K step inside the atom
-            const uint64_t dah = umma_desc_sw128(ah + 32 * ks), dal = umma_desc_sw128(al + 32 * ks);
-            const uint64_t dwh = umma_desc_sw128(wh + 32 * ks), dwl = umma_desc_sw128(wl + 32 * ks);
-            umma_tf32(dcol, dah, dwh, idesc, ks > 0 ? 1u : 0u);
-            umma_tf32(dcol, dal, dwh, idesc, 1u);
-            umma_tf32(dcol, dah, dwl, idesc, 1u);
-          }
-          umma_commit(&s_mfree[b]);  // operand buffer free once these MMAs completed
-          umma_commit(&s_accf[r]);   // chunk result ready
-        }
-      }
-    }
-    return;
-  }
-
-  const int L = P.L, ncol = 2 * L;
-  if (warp >= K1T_CONV_WARPS) {
-    // ---------------- drain warps: thread = row = TMEM lane. Phase-rotated
-    // chunk sums are added in fp32 over K1T_FGRP chunks, then folded into fp64
-    // (every fp32 chain stays short, so the Parseval noise estimate keeps its
-    // precision); the item's partial bins go to global memory.
-    constexpr int K1T_FGRP = 4;
-    static_assert(LC <= NB && LC % 2 == 0, "2L output columns within the MMA N");
-    const int t = threadIdx.x - 32 * K1T_CONV_WARPS;
-    const uint32_t lane_base = tmem + ((uint32_t)((warp - K1T_CONV_WARPS) * 32) << 16);
-    mbar_wait_spin(&s_w, 0);  // phase table landed
-    int j = 0;
-    for (int item = blockIdx.x; item < n_items; item += G) {
-      int g, d, c0, c1;
-      item_chunks(item, g, d, c0, c1);
-      const int row = g * 128 + t;
-      float acc[LC];
-      double acc64[LC];
-#pragma unroll
-      for (int q = 0; q < LC; ++q) acc[q] = 0.f, acc64[q] = 0.0;
-      for (int c = c0; c < c1; ++c, ++j) {
-        const int r = j % K1T_ACC;
-        {
-          mbar_wait_spin(&s_accf[r], (j / K1T_ACC) & 1);
-        }
+      for (int item = i_begin, j = 0; item < i_end; ++item, ++j) {
+        const int b = j % K1T_MBUF, r = j % K1T_ACC;
+        if (j >= K1T_ACC) mbar_wait_spin(&s_acce[r], ((j / K1T_ACC) - 1) & 1);
+        mbar_wait_spin(&s_conv[b], (j / K1T_MBUF) & 1);
+        K1TR(4, j, true);
         tc_fence_after();
-        float vals[NB];
-        tmem_ld_n<NB>(lane_base + (uint32_t)(r * nb), vals);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        mbar_arrive(&s_acce[r]);
-        const float2* ph = rotsm + (size_t)c * (LC / 2);
+        const uint32_t dcol = tmem + (uint32_t)(r * nb);
+        const uint32_t ah = smem_u32(mbuf + (size_t)b * 2 * K1T_OP_BYTES), al = ah + K1T_OP_BYTES;
 #pragma unroll
-        for (int l = 0; l < LC / 2; ++l) {
-          const float2 v = cmul(make_float2(vals[2 * l], vals[2 * l + 1]), ph[l]);
-          acc[2 * l] += v.x;
-          acc[2 * l + 1] += v.y;
+        for (int ks = 0; ks < 4; ++ks) {  // 8 tf32 (32 B) per K step inside the atom
+          const uint64_t dah = umma_desc_sw128(ah + 32 * ks), dal = umma_desc_sw128(al + 32 * ks);
+          const uint64_t dwh = umma_desc_sw128(wh + 32 * ks), dwl = umma_desc_sw128(wl + 32 * ks);
+          umma_tf32(dcol, dah, dwh, idesc, ks > 0 ? 1u : 0u);
+          umma_tf32(dcol, dal, dwh, idesc, 1u);
+          umma_tf32(dcol, dah, dwl, idesc, 1u);
         }
-        if ((c - c0) % K1T_FGRP == K1T_FGRP - 1 || c + 1 == c1) {
-#pragma unroll
-          for (int q = 0; q < LC; ++q) {
-            acc64[q] += (double)acc[q];
-            acc[q] = 0.f;
-          }
-        }
-      }
-      if (row < a.n_rows) {
-        double2* dst = reinterpret_cast<double2*>(a.dpart + ((size_t)item * 128 + t) * ncol);
-#pragma unroll
-        for (int q = 0; q < LC; q += 2) dst[q >> 1] = make_double2(acc64[q], acc64[q + 1]);
+        umma_commit(&s_mfree[b]);  // operand buffer free once these MMAs completed
+        umma_commit(&s_accf[r]);   // chunk result ready
       }
     }
-    tc_fence_before();
-    asm volatile("bar.arrive 2, %0;" ::"r"(2 * NT) : "memory");  // TMEM reads done
+    __syncwarp();
+    named_bar(2, NTMEM);  // the drains have read their last accumulator
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
     return;
   }
 
-  // ---------------- converter warps: thread = row
-  const int t = threadIdx.x;
-  const int pD = P.D;
-  // this row's SWIZZLE_128B positions of the 8 16-byte groups (byte offsets)
-  const uint32_t sw = (uint32_t)(t & 7);
-  uint32_t swz[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) swz[k] = ((uint32_t)k ^ sw) * 16u;
-  int j = 0;
-  for (int item = blockIdx.x; item < n_items; item += G) {
-    int g, d, c0, c1;
-    item_chunks(item, g, d, c0, c1);
-    const int row = g * 128 + t;
-    const bool live = row < a.n_rows;
-    const int stream = live ? (row / P.A) / a.n_slots : 0;
-    const float2* pl = a.pil + (size_t)stream * P.M * P.D + d;
-    double e64 = 0.0;
-    // comb pilots, one chunk ahead of the conversion
-    float2 qn[K1T_CP];
-    auto load_pilots = [&](int c) {
-      const int mlim = (live && c < c1) ? min(K1T_CP, P.M - c * K1T_CP) : 0;
-      const float2* pc = pl + (size_t)c * K1T_CP * pD;  // this chunk's first comb point
-#pragma unroll
-      for (int k = 0; k < K1T_CP; ++k) {
-        qn[k] = k < mlim ? __ldg(pc) : make_float2(0.f, 0.f);
-        pc += pD;
-      }
-    };
-    load_pilots(c0);
-    for (int c = c0; c < c1; ++c, ++j) {
-      const int s = j % K1T_STAGES, b = j % K1T_MBUF;
-      float2 qv[K1T_CP];
-#pragma unroll
-      for (int k = 0; k < K1T_CP; ++k) qv[k] = qn[k];
-      load_pilots(c + 1);
-      {
-        mbar_wait_spin(&s_full[s], (j / K1T_STAGES) & 1);
-      }
-      {
-        if (j >= K1T_MBUF) mbar_wait_spin(&s_mfree[b], ((j / K1T_MBUF) - 1) & 1);
-      }
-      // row t, 16-byte group k of atom a at a*16K + t*128 + (k ^ (t & 7))*16
-      // (SWIZZLE_128B); group = (y[2m].re, .im, y[2m+1].re, .im), m = 16c + 8a + k
-      const unsigned char* src = raw + (size_t)s * K1T_RAW_BYTES + t * 128;
-      unsigned char* ah = mbuf + (size_t)b * 2 * K1T_OP_BYTES + t * 128;
-      unsigned char* al = ah + K1T_OP_BYTES;
-      float2 hv[K1T_CP];
-      float e32 = 0.f;
-#pragma unroll
-      for (int k = 0; k < K1T_CP; ++k) {
-        const float4 v = *reinterpret_cast<const float4*>(src + (k >> 3) * K1T_ATOM + swz[k & 7]);
-        const float2 p = qv[k];
-        const float n2 = p.x * p.x + p.y * p.y;
-        float inv;  // 1/|p|^2 within 1 ulp (exact for the unit-modulus QPSK pilots); 0 for padding
-        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(n2));
-        inv = n2 > 0.f ? inv : 0.f;
-        hv[k] = make_float2((p.x * v.x + p.y * v.y) * inv, (p.x * v.y - p.y * v.x) * inv);
-        e32 = fmaf(hv[k].x, hv[k].x, fmaf(hv[k].y, hv[k].y, e32));
-      }
-      // compacted operand: group k' holds comb points 2k', 2k'+1 (tf32 hi | lo)
-#pragma unroll
-      for (int k = 0; k < K1T_CP / 2; ++k) {
-        const float2 h0 = hv[2 * k], h1 = hv[2 * k + 1];
-        const float4 hi = make_float4(tf32_rna_fast(h0.x), tf32_rna_fast(h0.y), tf32_rna_fast(h1.x),
-                                      tf32_rna_fast(h1.y));
-        *reinterpret_cast<float4*>(ah + swz[k]) = hi;
-        // lo = h - hi is exact in fp32 (<= 14 significant bits); the MMA reads its
-        // top 11, so the dropped tail is < 2^-22 |h| -- no explicit rounding needed
-        *reinterpret_cast<float4*>(al + swz[k]) = make_float4(h0.x - hi.x, h0.y - hi.y, h1.x - hi.z, h1.y - hi.w);
-      }
-      // raw stage consumed: every loaded value has been used above, so the
-      // TMA refill cannot race the shared-memory reads
-      mbar_arrive(&s_empty[s]);
-      e64 += (double)e32;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&s_conv[b]);
-    }
-    if (live) a.epart[(size_t)item * 128 + t] = e64;
+  if (warp >= K1T_CONV_WARPS) {
+    // ---------------- drain warps: warps 4-7 columns [0, 24), warps 8-11 [24, 2L)
+    static_assert(LC <= NB && LC % 2 == 0 && LC > 24, "2L output columns within the MMA N");
+    const int t = (warp & 3) * 32 + lane;  // MMA row = TMEM lane
+    named_bar(1, NTMEM);                   // the MMA warp's TMEM allocation
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    K1TS(4, warp == K1T_CONV_WARPS && lane == 0);
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    mbar_wait_spin(&s_w, 0);  // phase table landed
+    if (warp < K1T_CONV_WARPS + 4)
+      k1t_drain<24, 0>(a, P.L, t, lane_base, rotsm, s_accf, s_acce, i_begin, i_end, nc, D);
+    else
+      k1t_drain<LC - 24, 24>(a, P.L, t, lane_base, rotsm, s_accf, s_acce, i_begin, i_end, nc, D);
+    K1TS(2, warp == K1T_CONV_WARPS && lane == 0);
+    tc_fence_before();
+    asm volatile("bar.arrive 2, %0;" ::"r"(NTMEM) : "memory");  // TMEM reads done
+    return;
   }
-  // TMEM is released once the drain warps have read their last accumulator
-  named_bar(2, 2 * NT);
-  tc_fence_after();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+
+  // ---------------- converter warps
+  const int tau = threadIdx.x;
+  const int c = tau & 7, rr = ((tau >> 3) + c) & (K1T_RR - 1);
+  const int t = rr * K1T_SUBS + c;  // the MMA row this thread converts
+  const int M = P.M;
+  double e64 = 0.0;
+  int seg = i_begin;
+  K1TItem it;
+  it.init(i_begin, nc, D);
+  // this thread's pilot of the next chunk: comb point tau of it
+  auto load_pilot = [&](const K1TItem& x, bool in_range) {
+    const int stream = x.g / a.gps;
+    const int m = x.ch * (K1T_CP * K1T_SUBS) + tau;
+    return in_range && m < M ? __ldg(a.pil + ((size_t)stream * M + m) * D + x.d) : make_float2(0.f, 0.f);
+  };
+  float2 pn = load_pilot(it, i_begin < i_end);
+  for (int item = i_begin, j = 0; item < i_end; ++item, ++j) {
+    const int s = j % K1T_STAGES, b = j % K1T_MBUF;
+    {
+      // pilot inverse conj(p)/|p|^2 of comb point tau (1/|p|^2 within 1 ulp,
+      // exact for the unit-modulus QPSK pilots; 0 past M)
+      const float2 p = pn;
+      const float n2 = p.x * p.x + p.y * p.y;
+      float inv;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(n2));
+      inv = n2 > 0.f ? inv : 0.f;
+      s_q[j & 1][(tau >> 4) * K1T_QP + (tau & 15)] = make_float2(p.x * inv, -p.y * inv);
+    }
+    K1TItem nx = it;
+    nx.next(nc, D);
+    pn = load_pilot(nx, item + 1 < i_end);
+    named_bar(3, NT);  // the chunk's pilot inverses are visible
+    mbar_wait_spin(&s_full[s], (j / K1T_STAGES) & 1);
+    K1TR(1, j, tau == 0);
+    if (j >= K1T_MBUF) mbar_wait_spin(&s_mfree[b], ((j / K1T_MBUF) - 1) & 1);
+    K1TR(2, j, tau == 0);
+    // 16-byte group k of the sub-chunk = (y[2m].re, .im, y[2m+1].re, .im), m = 16c + k;
+    // only the comb half (.x, .y) is read
+    const unsigned char* src = raw + (size_t)s * K1T_RAW_BYTES + rr * K1T_ROWP + c * (2 * K1T_CP * 8);
+    const float4* qs = reinterpret_cast<const float4*>(&s_q[j & 1][c * K1T_QP]);
+    unsigned char* ah = mbuf + (size_t)b * 2 * K1T_OP_BYTES + t * 128;
+    unsigned char* al = ah + K1T_OP_BYTES;
+    float e32 = 0.f;
+#pragma unroll
+    for (int k = 0; k < K1T_CP / 2; ++k) {
+      const float2 y0 = *reinterpret_cast<const float2*>(src + (2 * k) * 16);
+      const float2 y1 = *reinterpret_cast<const float2*>(src + (2 * k + 1) * 16);
+      const float4 q = qs[k];
+      const float2 h0 = make_float2(fmaf(y0.x, q.x, -y0.y * q.y), fmaf(y0.x, q.y, y0.y * q.x));
+      const float2 h1 = make_float2(fmaf(y1.x, q.z, -y1.y * q.w), fmaf(y1.x, q.w, y1.y * q.z));
+      e32 = fmaf(h0.x, h0.x, fmaf(h0.y, h0.y, e32));
+      e32 = fmaf(h1.x, h1.x, fmaf(h1.y, h1.y, e32));
+      const float4 hi = make_float4(tf32_rna_fast(h0.x), tf32_rna_fast(h0.y), tf32_rna_fast(h1.x),
+                                    tf32_rna_fast(h1.y));
+      const uint32_t o = (uint32_t)((k ^ c) * 16);  // SWIZZLE_128B: group k of row t at (k ^ (t & 7))
+      *reinterpret_cast<float4*>(ah + o) = hi;
+      // lo = h - hi is exact in fp32 (<= 14 significant bits); the MMA reads its
+      // top 11, so the dropped tail is < 2^-22 |h| -- no explicit rounding needed
+      *reinterpret_cast<float4*>(al + o) = make_float4(h0.x - hi.x, h0.y - hi.y, h1.x - hi.z, h1.y - hi.w);
+    }
+    // raw stage consumed: every loaded value has been used above, so the
+    // copy refill cannot race the shared-memory reads
+    mbar_arrive(&s_empty[s]);
+    e64 += (double)e32;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive(&s_conv[b]);
+    K1TR(3, j, tau == 0);
+    if (item + 1 == i_end || it.ch + 1 == nc) {
+      // segment end: the data row's 8 sub-chunk energies, summed in sub-chunk order
+      s_e[t] = e64;
+      named_bar(3, NT);
+      if (tau < K1T_RR) {
+        const int stream = it.g / a.gps, lrow = (it.g - stream * a.gps) * K1T_RR + tau;
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < K1T_SUBS; ++k) v += s_e[tau * K1T_SUBS + k];
+        if (lrow < a.srows) a.epart[(size_t)seg * K1T_RR + tau] = v;
+      }
+      e64 = 0.0;
+      seg = item + 1;
+    }
+    it = nx;
+  }
 }
 
-// One CTA per unit: thread o sums output o (= (a, d, component)) over the parts
-// in part order (fp64, loads in flight together); warp 0 forms sigma2
+// Row `row`'s DMRS-symbol-d value (column cc of `ncol`) summed over its
+// segments in chunk order (K1's partials, written at segment starts: the row
+// tile's first chunk and every CTA range start inside the tile)
+__device__ __forceinline__ double k1t_row_sum(const K1TArgs& a, const double* part, int ncol, int row,
+                                              int d, int D, int cc) {
+  const int stream = row / a.srows, lrow = row - stream * a.srows;
+  const int g = stream * a.gps + lrow / K1T_RR, r = lrow % K1T_RR;
+  const int i0 = (g * D + d) * a.n_chunks, i1 = i0 + a.n_chunks;
+  double sum = __ldcg(part + ((size_t)i0 * K1T_RR + r) * ncol + cc);
+  for (int b = k1t_owner(i0, a.n_items, a.grid) + 1;; ++b) {
+    const int i = k1t_first(b, a.n_items, a.grid);
+    if (i >= i1) break;
+    sum += __ldcg(part + ((size_t)i * K1T_RR + r) * ncol + cc);
+  }
+  return sum;
+}
+
+// One CTA per unit: thread o sums output o (= (a, d, component)) over its row's
+// segments in chunk order (fp64); every thread forms sigma2
 // (Parseval), then the MMSE and AI taps.
 #define K1T_FIN_THREADS 512
 __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev P, const K1TArgs a,
@@ -382,33 +531,19 @@ __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize(const PlanDev 
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int L = P.L, ncol = 2 * L, AD = P.A * P.D, nout = AD * ncol;
   double* acc = nout <= 4096 ? s_bins : o.parts + (size_t)u * (2 * (size_t)AD * L + 2);
-  const int np = a.parts;
-  const size_t pstride = (size_t)P.D * a.n_g * 128 * ncol;  // next part, same (d, g, row)
   double sg = 0.0;  // this thread's share of sum_{a,d,l<guard} |B_l|^2
   for (int o2 = tid; o2 < nout; o2 += K1T_FIN_THREADS) {
     const int ad = o2 / ncol, cc = o2 - ad * ncol;
     const int aa = ad / P.D, d = ad - aa * P.D;
-    const int row = u * P.A + aa, g = row / 128, r = row - g * 128;
-    const double* src = a.dpart + ((size_t)(d * a.n_g + g) * 128 + r) * ncol + cc;
-    double sum = 0.0;
-    for (int q0 = 0; q0 < np; q0 += 8) {
-      double v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = q0 + k < np ? __ldcg(src + (size_t)(q0 + k) * pstride) : 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) sum += v[k];
-    }
+    const double sum = k1t_row_sum(a, a.dpart, ncol, u * P.A + aa, d, P.D, cc);
     acc[o2] = sum;
     if (cc < 2 * P.guard) sg += sum * sum;
   }
-  // row energies: thread = (a, d, part), every load in flight at once (a per-thread
-  // loop over the parts serialises one L2 round trip per part)
+  // row energies: thread = (a, d)
   double e = 0.0;
-  for (int o2 = tid; o2 < AD * np; o2 += K1T_FIN_THREADS) {
-    const int ad = o2 / np, q = o2 - ad * np;
+  for (int ad = tid; ad < AD; ad += K1T_FIN_THREADS) {
     const int aa = ad / P.D, d = ad - aa * P.D;
-    const int row = u * P.A + aa, g = row / 128, r = row - g * 128;
-    e += __ldcg(a.epart + (size_t)((q * P.D + d) * a.n_g + g) * 128 + r);
+    e += k1t_row_sum(a, a.epart, 1, u * P.A + aa, d, P.D, 0);
   }
   e = warp_sum(e);
   sg = warp_sum(sg);
@@ -463,31 +598,18 @@ __global__ void __launch_bounds__(K1T_FIN_THREADS) k1_tc_finalize_rows(const Pla
   const int L = P.L, ncol = 2 * L, AD = P.A * P.D;
   const int r0 = c * K1T_FIN_ROWS, r1 = min(AD, r0 + K1T_FIN_ROWS);
   double* acc = o.parts + (size_t)u * (2 * (size_t)AD * L + 2);
-  const int np = a.parts;
-  const size_t pstride = (size_t)P.D * a.n_g * 128 * ncol;
   double sg = 0.0;
   for (int o2 = r0 * ncol + tid; o2 < r1 * ncol; o2 += K1T_FIN_THREADS) {
     const int ad = o2 / ncol, cc = o2 - ad * ncol;
     const int aa = ad / P.D, d = ad - aa * P.D;
-    const int row = u * P.A + aa, g = row / 128, r = row - g * 128;
-    const double* src = a.dpart + ((size_t)(d * a.n_g + g) * 128 + r) * ncol + cc;
-    double sum = 0.0;
-    for (int q0 = 0; q0 < np; q0 += 8) {
-      double v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = q0 + k < np ? __ldcg(src + (size_t)(q0 + k) * pstride) : 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) sum += v[k];
-    }
+    const double sum = k1t_row_sum(a, a.dpart, ncol, u * P.A + aa, d, P.D, cc);
     __stcg(&acc[o2], sum);
     if (cc < 2 * P.guard) sg += sum * sum;
   }
   double e = 0.0;
-  for (int o2 = tid; o2 < (r1 - r0) * np; o2 += K1T_FIN_THREADS) {
-    const int ad = r0 + o2 / np, q = o2 % np;
+  for (int ad = r0 + tid; ad < r1; ad += K1T_FIN_THREADS) {
     const int aa = ad / P.D, d = ad - aa * P.D;
-    const int row = u * P.A + aa, g = row / 128, r = row - g * 128;
-    e += __ldcg(a.epart + (size_t)((q * P.D + d) * a.n_g + g) * 128 + r);
+    e += k1t_row_sum(a, a.epart, 1, u * P.A + aa, d, P.D, 0);
   }
   e = warp_sum(e);
   sg = warp_sum(sg);
