@@ -471,17 +471,24 @@ def run_ours(a, rank, world, backend):
     nv_h = torch.from_numpy(nv).pin_memory()
     reg_h = torch.from_numpy(reg).pin_memory()
     kpm_h = torch.empty(eng.kpm.numel(), dtype=torch.uint8).pin_memory()
+    # double-buffered: stage() copies step n+1's inputs into the engine's idle input
+    # set on its copy stream while step n runs (run_staged); every step's inputs
+    # still cross PCIe inside the timed region
     for _ in range(2):
-        eng.load(y=y_h, tx=tx_h, noise_var=nv_h, regime=reg_h, non_blocking=True)
-        eng.run()
+        eng.stage(y_h, tx_h, nv_h, reg_h)
+        eng.run_staged()
         kpm_h.copy_(eng.kpm, non_blocking=True)
+    torch.cuda.synchronize()
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record()
-    for _ in range(K):
-        eng.load(y=y_h, tx=tx_h, noise_var=nv_h, regime=reg_h, non_blocking=True)
-        eng.run()
+    eng._copy_stream.wait_stream(torch.cuda.current_stream())  # step 0's copy starts after e2
+    eng.stage(y_h, tx_h, nv_h, reg_h)
+    for k in range(K):
+        eng.run_staged()
         kpm_h.copy_(eng.kpm, non_blocking=True)
+        if k + 1 < K:
+            eng.stage(y_h, tx_h, nv_h, reg_h)
     e3.record()
     barrier()
     te, e2e_units = reduce_metrics(e2.elapsed_time(e3), K * U, red_dev)
@@ -576,7 +583,8 @@ def run_ours(a, rank, world, backend):
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "how": "pinned host y (complex64) + tx (packed QPSK wire format, 2 bits/RE) + "
                            "noise_var + regime -> H2D -> " + ("" if packed else "unpack + ") +
-                           "run (graph) -> D2H KPM records, every step, one stream"},
+                           "run (eager, ordered executor) -> D2H KPM records, every step; "
+                           "double-buffered: step n+1's H2D on a copy stream overlaps step n"},
             "latency": lat,
             "gpu_launches": plan.batch_kernels() * K,  # RNG, K1, K1 finalize(s), K2, K3, K4 per step
             "clocks": clk,

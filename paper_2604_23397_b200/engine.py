@@ -345,6 +345,66 @@ class SlotEngine:
                                                 _lib.ptr(xh), _lib.ptr(lr), _stream_handle()))
         return xh, lr
 
+    # ------------------------------------------------------------ double-buffered inputs
+    def stage(self, y, tx, noise_var, regime):
+        """Copy the NEXT batch's inputs (pinned host tensors: y, tx as the complex
+        grid or the packed QPSK wire format, noise_var, regime) into the idle one
+        of two device input sets on the engine's copy stream; run_staged() then
+        processes them.  A set is refilled only after the run that read it, so the
+        host-to-device copy of batch n+1 overlaps the compute of batch n."""
+        import torch
+        if getattr(self, "_sets", None) is None:
+            dev = self.device
+            self._sets = [
+                dict(y=self.y, tx=self.tx, nv=self.noise_var, reg=self.regime, bits=None),
+                dict(y=torch.empty_like(self.y), tx=torch.empty_like(self.tx),
+                     nv=torch.empty_like(self.noise_var), reg=torch.empty_like(self.regime), bits=None)]
+            self._copy_stream = torch.cuda.Stream(device=dev)
+            self._copy_stream.wait_stream(torch.cuda.current_stream())
+            self._copied = [torch.cuda.Event(), torch.cuda.Event()]
+            self._read = [torch.cuda.Event(), torch.cuda.Event()]
+            self._cur = 0
+        idle = 1 - self._cur
+        st, cs = self._sets[idle], self._copy_stream
+        cs.wait_event(self._read[idle])  # the run that last read this set is done
+        shape_bits = (self.U, -(-self.N // 128), self.T, 32)
+        with torch.cuda.stream(cs):
+            for key, src in (("y", y), ("nv", noise_var), ("reg", regime)):
+                if tuple(src.shape) != tuple(st[key].shape):
+                    raise ContractViolation(f"shape {tuple(src.shape)}, expected {tuple(st[key].shape)}")
+                st[key].copy_(src, non_blocking=True)
+            if tx.dtype == torch.uint8 and not self.tx_packed:  # wire format, expanded in run_staged
+                if tuple(tx.shape) != shape_bits:
+                    raise ContractViolation(f"packed tx shape {tuple(tx.shape)}, expected {shape_bits}")
+                if st["bits"] is None:
+                    st["bits"] = torch.empty(shape_bits, dtype=torch.uint8, device=self.device)
+                st["bits"].copy_(tx, non_blocking=True)
+                st["unpack"] = True
+            else:
+                if tuple(tx.shape) != tuple(st["tx"].shape):
+                    raise ContractViolation(f"tx shape {tuple(tx.shape)}, expected {tuple(st['tx'].shape)}")
+                st["tx"].copy_(tx, non_blocking=True)
+                st["unpack"] = False
+            self._copied[idle].record(cs)
+        self._staged = idle
+
+    def run_staged(self):
+        """Process the batch stage() copied (eager ordered executor: a captured
+        graph holds the other set's pointers)."""
+        import torch
+        self._settle()
+        cur = self._staged
+        st = self._sets[cur]
+        torch.cuda.current_stream().wait_event(self._copied[cur])
+        self.y, self.tx, self.noise_var, self.regime = st["y"], st["tx"], st["nv"], st["reg"]
+        if st.get("unpack"):
+            _lib.check(_lib.lib().arches_unpack_qpsk(self.plan.handle, self.U, _lib.ptr(st["bits"]),
+                                                     _lib.ptr(self.tx), _stream_handle()))
+        self._launch(-1)
+        self._read[cur].record()
+        self._cur = cur
+        self.next_slot += self.S
+
     def join(self):
         """Order the current stream after any pending pipelined tail."""
         _lib.check(_lib.lib().arches_join(self.plan.handle, _stream_handle()))

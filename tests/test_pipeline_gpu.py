@@ -150,3 +150,36 @@ def test_streaming_load_between_pipelined_batches():
     for x, y in zip(out[0], out[1]):
         assert np.array_equal(x, y)
     assert len(out[0][1]) >= 8   # the regime timeline drove mode changes in every batch
+
+
+@pytest.mark.parametrize("wire", [False, True])
+def test_double_buffered_staging_matches_load_then_run(wire):
+    """SlotEngine.stage / run_staged (the bench's e2e loop: batch n+1's inputs cross
+    PCIe on a copy stream while batch n runs) give, batch by batch, exactly what
+    load + run give -- with a different input batch every step, so a stale or
+    swapped input set would show."""
+    import torch
+    from paper_2604_23397_b200.scene import pack_qpsk
+    geo = SlotGeometry(n_ant=4, n_prb=52)
+    ref = _engine(geo, 1, 16, ExecutionMode.CONCURRENT, [11])
+    dbl = _engine(geo, 1, 16, ExecutionMode.CONCURRENT, [11])
+    y0, tx0 = ref.y.cpu(), ref.tx.cpu()
+    nv0, reg0 = ref.noise_var.cpu(), ref.regime.cpu()
+    batches = []
+    for k in range(5):
+        tx = torch.from_numpy(pack_qpsk(tx0.numpy())) if wire else tx0.clone()
+        batches.append(tuple(t.pin_memory() for t in (
+            y0 * (1.0 + 0.15 * k), tx, nv0 * (1.0 + 0.05 * k), torch.roll(reg0, k))))
+    want = []
+    for b in batches:
+        ref.load(y=b[0], tx=b[1], noise_var=b[2], regime=b[3])
+        ref.run()
+        want.append(_snapshot(ref))
+    dbl.stage(*batches[0])
+    for k in range(len(batches)):
+        dbl.run_staged()
+        got = _snapshot(dbl)
+        if k + 1 < len(batches):
+            dbl.stage(*batches[k + 1])
+        for key in want[k]:
+            assert np.array_equal(got[key], want[k][key]), (k, key)
