@@ -117,6 +117,17 @@ static cudaError_t ensure_smem(K kern, size_t smem) {
   return e;
 }
 
+// SMs the persistent K1 / K2 grids use.  In the cross-batch pipeline a tree
+// (dApp) policy's control walk of the previous batch (K4 on the plan's tail
+// stream, tens of microseconds on one SM per stream) would otherwise hold an SM
+// that one of K2's statically partitioned CTAs waits for, stretching the whole
+// step: one SM is left to it (config A 4.83 -> 7.29 M slots/s; the same reserve
+// costs config B, whose K4 is short, 1%, so other plans keep every SM).
+static int persistent_sms(const PlanDev& d) {
+  const bool long_tail = g_hook.k3_stream != nullptr && d.policy == ARCHES_POLICY_TREE;
+  return std::max(1, d.num_sms - (long_tail ? 1 : 0));
+}
+
 // ------------------------------------------------------------ workspace
 struct WsLayout {
   size_t coef, parts, counters, k1parts, k1counters, sigma2, rng, k1t_d, k1t_e, k1t_share, total;
@@ -640,7 +651,7 @@ static K1TGeom k1t_geom(const arches_plan* P, int n_streams, int n_slots) {
   g.gps = (n_slots * d.A + K1T_RR - 1) / K1T_RR;
   g.n_g = n_streams * g.gps;
   g.n_items = g.n_g * d.D * P->k1t_nchunks;
-  g.grid = std::max(1, std::min(g.n_items, d.num_sms));
+  g.grid = std::max(1, std::min(g.n_items, persistent_sms(d)));
   return g;
 }
 
@@ -854,7 +865,7 @@ static int launch_k2_tc(const arches_plan* P, int n_units, const K2Args& a, cuda
   const PlanDev& d = P->dev;
   const int ngrp = P->k2_groups;
   const int n_items = n_units * d.n_tiles * ngrp;
-  const int grid = std::min(n_units * d.n_tiles, d.num_sms);  // persistent: one CTA per SM
+  const int grid = std::min(n_units * d.n_tiles, persistent_sms(d));  // persistent: one CTA per SM
   const size_t smem = P->k2_tc_smem;
   const int na = d.A <= 1 ? 1 : d.A <= 2 ? 2 : 4;
   const bool std_pat = d.T == 14 && d.D == 3 && d.dsym[0] == 0 && d.dsym[1] == 5 && d.dsym[2] == 10;
