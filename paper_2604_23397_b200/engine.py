@@ -351,8 +351,12 @@ class SlotEngine:
         grid or the packed QPSK wire format, noise_var, regime) into the idle one
         of two device input sets on the engine's copy stream; run_staged() then
         processes them.  A set is refilled only after the run that read it, so the
-        host-to-device copy of batch n+1 overlaps the compute of batch n."""
+        host-to-device copy of batch n+1 overlaps the compute of batch n.  For a
+        plan with ARCHES_FLAG_TX_PACKED, tx must already be the wire format.  A
+        graph captured earlier (capture_graph) holds one set's pointers: staging
+        drops it, later run() calls launch eagerly."""
         import torch
+        self.graph = None
         if getattr(self, "_sets", None) is None:
             dev = self.device
             self._sets = [
