@@ -25,14 +25,15 @@
 //     rr = (tau/8 + c) mod 16, c = tau mod 8 (a quarter warp reads 8 rows at 8
 //     bank offsets and writes 8 SWIZZLE_128B groups): h = y q, tf32 hi | lo into
 //     one of two MMA operand buffers (the raw stage is released right away);
-//   * MMA warp: D = A_hi W_hi + A_lo W_hi + A_hi W_lo (kind::tf32, 3xTF32) into a
-//     ring of TMEM accumulators;
-//   * drain warps (thread = TMEM lane = MMA row): tcgen05.ld of the row's 2L
-//     columns, the sub-chunk phase, fp32 sums over 4 chunks folded into fp64
-//     (short fp32 chains keep the Parseval noise estimate precise); at a
-//     segment end (row tile change or the CTA's last chunk) the 8 sub-chunk
-//     lanes of a data row are summed (fp64 xor shuffles) and the segment's
-//     partial bins / row energy go to global memory.
+//   * MMA warp (owns the TMEM allocation): D = A_hi W_hi + A_lo W_hi + A_hi W_lo
+//     (kind::tf32, 3xTF32) into a ring of TMEM accumulators;
+//   * drain warps, two groups of 4 (columns [0, 24) and [24, 2L); thread = TMEM
+//     lane = MMA row): tcgen05.ld, the sub-chunk phase, fp32 sums over 4 chunks
+//     folded into fp64 (short fp32 chains keep the Parseval noise estimate
+//     precise); at a segment end (row tile change or the CTA's last chunk) a
+//     reduce-scatter over the data row's 8 sub-chunk lanes (fp64 shuffles) and
+//     the segment's partial bins go to global memory (the converters sum the
+//     row energies through shared memory).
 // Work split: the (row tile, DMRS symbol, chunk) items in that order, cut into
 // one contiguous range per CTA (balanced to one chunk); the finalize sums a
 // row's segments in chunk order, a segment starting at chunk 0 or at a CTA's
