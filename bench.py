@@ -73,9 +73,10 @@ def parse(argv=None):
     ap.add_argument("--mode", default="pipeline", choices=["pipeline", "policy-stress"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--latency-slots", type=int, default=400)
-    ap.add_argument("--tx", default="complex", choices=["packed", "complex"],
-                    help="resident genie-tx format: the complex64 grid, or 2-bit QPSK codes read "
-                         "by K2 (ARCHES_FLAG_TX_PACKED, n_ant 1/2/4)")
+    ap.add_argument("--tx", default="packed", choices=["packed", "complex"],
+                    help="resident genie-tx format: 2-bit QPSK codes read by K2 "
+                         "(ARCHES_FLAG_TX_PACKED, n_ant 1/2/4; other plans fall back to the grid), "
+                         "or the complex64 grid")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sequential", action="store_true",
                     help="one CUDA graph per step, no cross-batch pipeline (arches_run_batch)")
@@ -454,7 +455,8 @@ def run_ours(a, rank, world, backend):
     if os.path.exists(tpath):  # dram__bytes_read + write per K2 launch, from a committed ncu capture
         entries = json.load(open(tpath))
         for tj in entries if isinstance(entries, list) else [entries]:
-            if tj.get("n_prb") == a.n_prb and tj.get("n_ant") == A and tj.get("units") == U:
+            if (tj.get("n_prb") == a.n_prb and tj.get("n_ant") == A and tj.get("units") == U
+                    and tj.get("tx", "complex") == ("packed" if packed else "complex")):
                 traffic = tj["bytes_per_launch"]
                 traffic_src = (f"committed ncu capture ({os.path.relpath(tpath, ROOT)}, "
                                f"{tj.get('captured', 'this config')}), not measured in this run")

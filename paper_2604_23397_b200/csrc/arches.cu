@@ -546,7 +546,7 @@ extern "C" int arches_plan_create(const arches_geom* geom, const arches_params* 
       // two y (+ tx) stages; antenna groups keep the tile's tx rows in one extra buffer;
       // packed tx: the tile's 2-bit codes (padded to 512 B) instead of its tx rows
       sm = (p.flags & ARCHES_FLAG_TX_PACKED)
-               ? 2 * ((size_t)as * d.T * ARCHES_TILE * sizeof(float2) + 512)
+               ? 3 * ((size_t)as * d.T * ARCHES_TILE * sizeof(float2) + 512)  // k2_tc NST = 3
                : (2 * (size_t)(as + (grp ? 0 : 1)) + (grp ? 1 : 0)) * d.T * ARCHES_TILE * sizeof(float2);
       sm += 2 * nbuf * (size_t)d.tc_kb * ng * 256;
       if (grp) sm += (size_t)21 * TC_THREADS * sizeof(float);  // MRC sums across groups

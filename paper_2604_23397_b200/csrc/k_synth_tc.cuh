@@ -367,8 +367,9 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
   // Antenna-group plans (longer epilogue, 96 registers would spill under a 17th
   // warp): the last epilogue warp to complete a B operand issues them itself
   constexpr bool kProd = !kGrp;
+  constexpr int NST = kPk ? 3 : 2;  // y / tx stages (packed tx leaves room for a third)
   extern __shared__ __align__(128) unsigned char sm[];
-  __shared__ __align__(8) uint64_t s_full[2];       // stage landed
+  __shared__ __align__(8) uint64_t s_full[3];       // stage landed
   __shared__ __align__(8) uint64_t s_mma[NBUF];     // accumulator ready
   __shared__ __align__(8) uint64_t s_bready[NBUF];  // B(i) written (512 thread / 16 warp arrivals)
   __shared__ uint32_t s_bcount[NBUF];               // warps arrived on B(i) (!kProd: elects the issuer)
@@ -402,9 +403,9 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
   const size_t stage_elems = kPk ? (size_t)AS * T * ARCHES_TILE + 64
                                  : (size_t)(AS + (kGrp ? 0 : 1)) * T * ARCHES_TILE;
   const size_t coef_stride = coef_floats2(P);
-  float2* sYX = reinterpret_cast<float2*>(sm);                               // [2][stage]
-  float2* sX = sYX + 2 * stage_elems;                                         // [T][TILE] (kGrp)
-  unsigned char* sB = sm + (2 * stage_elems + (kGrp ? (size_t)T * ARCHES_TILE : 0)) * sizeof(float2);
+  float2* sYX = reinterpret_cast<float2*>(sm);                               // [NST][stage]
+  float2* sX = sYX + NST * stage_elems;                                       // [T][TILE] (kGrp)
+  unsigned char* sB = sm + (NST * stage_elems + (kGrp ? (size_t)T * ARCHES_TILE : 0)) * sizeof(float2);
   float* gacc = reinterpret_cast<float*>(sB + 2 * NBUF * (size_t)KB * NG * 256) + threadIdx.x;  // [21][512] (kGrp)
   float2* srot = reinterpret_cast<float2*>(sB + 2 * NBUF * (size_t)KB * NG * 256 +
                                            (kGrp ? (size_t)21 * TC_THREADS * sizeof(float) : 0));  // [n_tiles][L4+8]
@@ -437,8 +438,7 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
   }
 
   if (threadIdx.x == 0) {
-    mbar_init(&s_full[0], 1);
-    mbar_init(&s_full[1], 1);
+    for (int k = 0; k < NST; ++k) mbar_init(&s_full[k], 1);
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&s_mma[b], 1);
       mbar_init(&s_bready[b], kProd ? TC_THREADS : TC_THREADS / 32);
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
     // item j - NBUF), and the stage item j - LEAD used is refilled with item
     // j - LEAD + 2.  The epilogue warps never meet at a CTA barrier for this.
     int tu = u, tt = tile, tg = gr;  // next item to load
-    for (int k = 0; k < 2 && k < count; ++k) {
+    for (int k = 0; k < NST && k < count; ++k) {
       issue_tma(tu, tt, tg, k);
       advance(tu, tt, tg);
     }
@@ -596,9 +596,9 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
       mbar_wait(&s_bready[jj % NBUF], (jj / NBUF) & 1);
       if (lane == 0) issue_mma(jj % NBUF);
       __syncwarp();
-      const int nx = jj - LEAD + 2;
-      if (nx >= 2 && nx < count) {
-        issue_tma(tu, tt, tg, nx & 1);
+      const int nx = jj - LEAD + NST;
+      if (nx >= NST && nx < count) {
+        issue_tma(tu, tt, tg, nx % NST);
         advance(tu, tt, tg);
       }
     }
@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
   int seg_t0 = tile;  // first tile of the current (CTA, unit) segment
   float nv = lo < hi ? (float)__ldg(&args.nv[u]) : 0.f;
   for (int item = lo, i = 0; item < hi; ++item, ++i) {
-    const int buf = i & 1, ph = (i >> 1) & 1;       // y / tx stage
+    const int buf = i % NST, ph = (i / NST) & 1;    // y / tx stage
     const int mb = i % NBUF, mph = (i / NBUF) & 1;  // B operand + TMEM accumulator
     const bool has_next = item + 1 < hi;
     const bool has_lead = item + LEAD < hi;
@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
         }
       }
     }
-    // ---- end of a (CTA, unit) segment: per-warp partials -> s_red[buf]
+    // ---- end of a (CTA, unit) segment: per-warp partials -> s_red[i & 1] (item parity)
     if (flush) {
       const int col = half * 4 + q4;
       const double r2 = warp_sum((double)sre), r3 = warp_sum((double)sim);
@@ -756,16 +756,16 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
       if (ex == 0) r5 = warp_sum((double)sxx);
       if (lane == 0) {
         if (half == 1) {
-          s_red[buf][0 + ex][q4] = r0;
-          s_red[buf][2 + ex][q4] = r1;
+          s_red[i & 1][0 + ex][q4] = r0;
+          s_red[i & 1][2 + ex][q4] = r1;
         }
-        if (ex == 0) s_red[buf][4][col] = r5;
-        s_red[buf][5 + ex][col] = r2;
-        s_red[buf][7 + ex][col] = r3;
-        s_red[buf][9 + ex][col] = r4;
+        if (ex == 0) s_red[i & 1][4][col] = r5;
+        s_red[i & 1][5 + ex][col] = r2;
+        s_red[i & 1][7 + ex][col] = r3;
+        s_red[i & 1][9 + ex][col] = r4;
       }
       sa = sp = sre = sim = syy = sxx = 0.f;
-      named_bar(1, TC_THREADS);  // every warp's partials in s_red[buf]
+      named_bar(1, TC_THREADS);  // every warp's partials in s_red[i & 1]
     }
     // ---- B(i + LEAD) -> shared memory; signals the producer / MMA warp
     if (has_lead) {
@@ -776,10 +776,10 @@ __global__ void __launch_bounds__(kGrp ? TC_THREADS : TC_BLOCK, 1)
     if (flush && warp == 1 && lane < 11) {
       double acc;
       if (lane < 4) {  // abs / pow: half 1 only
-        acc = ((s_red[buf][lane][0] + s_red[buf][lane][1]) + s_red[buf][lane][2]) + s_red[buf][lane][3];
+        acc = ((s_red[i & 1][lane][0] + s_red[i & 1][lane][1]) + s_red[i & 1][lane][2]) + s_red[i & 1][lane][3];
       } else {
         acc = 0.0;
-        for (int w = 0; w < 8; ++w) acc += s_red[buf][lane][w];
+        for (int w = 0; w < 8; ++w) acc += s_red[i & 1][lane][w];
       }
       reinterpret_cast<double*>(args.parts + (size_t)u * n_tiles + seg_t0)[lane] = acc;
     }

@@ -13,6 +13,6 @@ timeout 900 python bench.py --cells 8 --layers 2 --slots 16 --no-cpu-baseline > 
 timeout 900 python bench.py --mode policy-stress --steps 200 > $O/bench_D.json 2> $O/bench_D.err
 timeout 900 python bench.py --n-ant 64 --layers 4 --slots 8 --no-cpu-baseline --latency-slots 0 > $O/bench_E.json 2> $O/bench_E.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --latency-slots 0 > $O/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_tc|k2_tc|k1_tc_finalize" -s 3 -c 3 -o $O/prof_B python tools/profile_step.py --slots 256 --steps 3 > $O/ncu_B.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_tc|k2_tc|k1_tc_finalize" -s 3 -c 3 -o $O/prof_B python tools/profile_step.py --slots 256 --steps 3 --tx packed > $O/ncu_B.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k2_tc|k1_tc" -s 2 -c 2 -o $O/prof_E python tools/profile_step.py --n-ant 64 --streams 4 --slots 8 --steps 2 > $O/ncu_E.log 2>&1
 tail -n 2 $O/smoke.log $O/pytest_gpu.log; for f in B ref A C D E; do tail -c 300 $O/bench_$f.json; echo; done
